@@ -1,0 +1,178 @@
+/*
+ * ivk.h -- C ABI of the B200-native IRK-Vanka hot path (libivk.so, sm_100a).
+ *
+ * The reference (`irkmg`, /root/reference/pkg/src/irkmg) is pure Python on
+ * numpy/scipy and has no FFI; its "operator interface" is the duck-typed
+ * Python API of stages.py / solvers.py.  Each entry point below replaces one
+ * reference call site on that path (cited file:line, paths relative to
+ * /root/reference/pkg/src/irkmg/).  The Python host layer
+ * (paper_2202_07381_b200/) binds these with ctypes and keeps the reference's
+ * Python signatures; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - All pointers except descriptors are DEVICE pointers owned by the caller
+ *    (torch allocations); the library never allocates or frees them.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t, passed as void*;
+ *    NULL = legacy default stream) and returns 0 or a negative IVK_E* code;
+ *    ivk_last_error() gives a message (thread-local).
+ *  - fp64 values, int32 indices, int64 offsets into the patch-inverse store.
+ *  - Vectors are in the reference's stage-major layout
+ *    [(u_1, p_1), ..., (u_s, p_s)], u interleaving the two velocity
+ *    components per scalar P2 node (stages.py:100-106, fem.py:9-13).
+ *  - Not thread-safe per descriptor; descriptors are plain structs.
+ */
+#ifndef IVK_H
+#define IVK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IVK_OK 0
+#define IVK_EINVAL (-1)
+#define IVK_ECUDA (-2)
+#define IVK_ESINGULAR (-3)
+#define IVK_EUNSUPPORTED (-4)
+
+#define IVK_MAX_STAGES 3
+
+/* Stage-coupled operator  I_s (x) diag(M, 0) + dt A (x) [[K, B], [B^T, 0]]
+ * (+ dt a_ij J_i on the velocity block), with identity rows on constrained
+ * velocity DoFs.  Replaces StageSystem.__init__/matvec (stages.py:63-126).
+ * M, K, J are stored on the scalar P2 pattern already eliminated (zero in
+ * constrained rows/columns, stages.py:77-85); B rows are per scalar node with
+ * (B_x, B_y) pairs, B^T rows per P1 node -- both eliminated. */
+typedef struct ivk_operator_desc {
+  int32_t stages;          /* s, 1..IVK_MAX_STAGES                        */
+  int32_t n_nodes;         /* scalar P2 nodes; n_u = 2 * n_nodes          */
+  int32_t n_p;             /* P1 pressure nodes                           */
+  int32_t n_conv;          /* 0: Stokes; 1: one J for all stages; s: J_i  */
+  int32_t nnz;             /* scalar P2 pattern entries                   */
+  double dt;
+  double butcher_a[IVK_MAX_STAGES * IVK_MAX_STAGES]; /* row-major s x s   */
+  const int32_t* p2_rowptr; /* n_nodes + 1                                 */
+  const int32_t* p2_col;    /* nnz                                         */
+  const double* p2_mk;      /* nnz * 2: (m, k) per entry                   */
+  const double* conv;       /* n_conv * nnz * 4: (Jxx, Jxy, Jyx, Jyy)      */
+  const int32_t* b_rowptr;  /* n_nodes + 1                                 */
+  const int32_t* b_col;     /* nnz_b (P1 node)                             */
+  const double* b_val;      /* nnz_b * 2: (B_x, B_y)                       */
+  const int32_t* bt_rowptr; /* n_p + 1                                     */
+  const int32_t* bt_col;    /* nnz_b (scalar P2 node)                      */
+  const double* bt_val;     /* nnz_b * 2                                   */
+  const uint8_t* node_constrained; /* n_nodes: 1 = both components fixed   */
+} ivk_operator_desc;
+
+/* Vanka vertex-star patch set (solvers.py:116-222).  Patches are laid out
+ * in the reference's group order (size ascending, vertex ascending within a
+ * size, solvers.py:169-175).  Patch p owns idx[idx_off[p] .. idx_off[p+1])
+ * (its stage-major local DoF list, solvers.py:160-165) and an m x ld block
+ * of the inverse store at inv_off[p], holding Inv^T (inv[j*ld + i] =
+ * Inv[i][j]), ld = (m + 3) & ~3.  dof_ptr/dof_pos is the inverse map
+ * global DoF -> positions in the flat local[] array, ascending. */
+typedef struct ivk_patch_desc {
+  int32_t num_patches;
+  int32_t dim;             /* stage-system dimension                      */
+  int32_t max_m;
+  int32_t total_m;         /* sum of patch sizes                          */
+  const int32_t* idx_off;  /* num_patches + 1                             */
+  const int32_t* idx;      /* total_m                                     */
+  const int64_t* inv_off;  /* num_patches                                 */
+  double* inv;             /* inverse store                               */
+  const int32_t* dof_ptr;  /* dim + 1                                     */
+  const int32_t* dof_pos;  /* total_m                                     */
+  const int32_t* vertex;   /* num_patches: centre vertex                  */
+  const int32_t* node_off; /* num_patches + 1                             */
+  const int32_t* node;     /* free scalar P2 nodes of each patch, sorted  */
+} ivk_patch_desc;
+
+/* Nested P2/P1 transfer I_s (x) blockdiag(P_P2 (x) I_2, P_P1)
+ * (bench.py:187-194, fem.py:255-301), fine <- coarse, plus its transpose. */
+typedef struct ivk_transfer_desc {
+  int32_t stages;
+  int32_t nf_nodes, nf_p;  /* fine scalar P2 nodes, fine P1 nodes        */
+  int32_t nc_nodes, nc_p;  /* coarse                                     */
+  const int32_t *p2_rowptr, *p2_col; const double* p2_val;    /* nf rows */
+  const int32_t *p2t_rowptr, *p2t_col; const double* p2t_val; /* nc rows */
+  const int32_t *p1_rowptr, *p1_col; const double* p1_val;
+  const int32_t *p1t_rowptr, *p1t_col; const double* p1t_val;
+  const uint8_t* fine_constrained;   /* per fine scalar node            */
+  const uint8_t* coarse_constrained; /* per coarse scalar node          */
+} ivk_transfer_desc;
+
+/* Coarsest-level direct solve with fixed LU factors (CoarseSolver,
+ * solvers.py:271-292): P_r (A + Z Z^T) P_c = L U, L unit lower, both dense
+ * row-major n x n.  Solve: project pressure means, x = P_c U^-1 L^-1 P_r b,
+ * project again. */
+typedef struct ivk_coarse_desc {
+  int32_t n;               /* = stages * (n_u + n_p)                      */
+  int32_t stages, n_u, n_p;
+  const double* lower;     /* n x n                                       */
+  const double* upper;     /* n x n                                       */
+  const int32_t* perm_r;   /* (P_r b)[perm_r[i]] = b[i]                   */
+  const int32_t* perm_c;   /* x[i] = y[perm_c[i]]                         */
+} ivk_coarse_desc;
+
+const char* ivk_last_error(void);
+int ivk_version(void);
+/* Number of kernels this library launched since load (for gpu_launches). */
+int64_t ivk_launch_count(void);
+
+/* out = b - A x  (b != NULL), or out = A x (b == NULL).  out may alias b.
+ * Replaces StageSystem.matvec (stages.py:110-126) and the residuals at
+ * solvers.py:238,258,263,340. */
+int ivk_stage_apply(const ivk_operator_desc* op, const double* x, const double* b,
+                    double* out, void* stream);
+
+/* local[idx_off[p] + i] = sum_j Inv_p[i][j] * r[idx[idx_off[p] + j]]
+ * (gather + batched patch solve: einsum at solvers.py:219-220). */
+int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, void* stream);
+
+/* Deterministic scatter (bincount at solvers.py:221) fused with the update:
+ * z_d = sum over dof_pos of local; out_d = alpha * x_d + beta * w_d * z_d
+ * (x == NULL -> 0, w == NULL -> 1); if accum != NULL also accum_d += out_d.
+ * out may alias x. */
+int ivk_patch_combine(const ivk_patch_desc* pd, const double* local, const double* x,
+                      double alpha, double beta, const double* w, double* out,
+                      double* accum, void* stream);
+
+/* Assemble every patch matrix from the operator (solvers.py:186-212) and
+ * invert it in place into pd->inv (np.linalg.inv, solvers.py:177) by
+ * Gauss-Jordan with partial pivoting.  *singular_dev (device int32, set to
+ * INT32_MAX by the caller) receives the smallest singular patch vertex. */
+int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd,
+                     int32_t* singular_dev, void* stream);
+
+/* One additive Vanka sweep x_out = x + omega * W * sum_i R_i^T A_i^-1 R_i (b - A x)
+ * (apply_vanka, solvers.py:232-239); r and local are caller scratch
+ * (dim and total_m doubles).  w == NULL is the reference's unweighted sweep. */
+int ivk_vanka_sweep(const ivk_operator_desc* op, const ivk_patch_desc* pd,
+                    const double* x, const double* b, double omega, const double* w,
+                    double* r, double* local, double* x_out, void* stream);
+
+/* rc = (I_s (x) P)^T rf, constrained coarse rows zeroed (solvers.py:341-342). */
+int ivk_restrict(const ivk_transfer_desc* t, const double* rf, double* rc, void* stream);
+/* xf += (I_s (x) P) ec on unconstrained fine rows (solvers.py:343-346). */
+int ivk_prolong_add(const ivk_transfer_desc* t, const double* ec, double* xf, void* stream);
+
+/* x = CoarseSolver.solve(b) (solvers.py:284-287); b and x must not alias. */
+int ivk_coarse_solve(const ivk_coarse_desc* c, const double* b, double* x, void* stream);
+
+/* Per-stage pressure-mean removal in place (stages.py:174-178). */
+int ivk_project_pressure_means(int32_t stages, int32_t n_u, int32_t n_p, double* x,
+                               void* stream);
+/* out = alpha * x + beta * y (x or y may be NULL -> 0); out may alias. */
+int ivk_axpby(int64_t n, double alpha, const double* x, double beta, const double* y,
+              double* out, void* stream);
+/* out = 0 except out[d] = src[d] on constrained velocity DoFs (the z[cd] = r[cd]
+ * seeding of MGHierarchyOp.precondition, solvers.py:352-354). */
+int ivk_seed_constrained(int32_t stages, int32_t n_nodes, int32_t n_p,
+                         const uint8_t* node_constrained, const double* src,
+                         double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IVK_H */

@@ -1,0 +1,129 @@
+"""ctypes binding of libivk.so (include/ivk.h).
+
+The library is the ONLY compute path: if it is missing or fails to load,
+every operator raises -- there is no CPU fallback.
+"""
+
+import ctypes as C
+import os
+
+__all__ = ["lib", "check", "OperatorDesc", "PatchDesc", "TransferDesc", "CoarseDesc",
+           "IVK_MAX_STAGES", "IvkError", "SingularPatch"]
+
+IVK_MAX_STAGES = 3
+IVK_ESINGULAR = -3
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libivk.so")
+
+i32p = C.POINTER(C.c_int32)
+i64p = C.POINTER(C.c_int64)
+f64p = C.POINTER(C.c_double)
+u8p = C.POINTER(C.c_uint8)
+
+
+class IvkError(RuntimeError):
+    pass
+
+
+class SingularPatch(IvkError):
+    pass
+
+
+class OperatorDesc(C.Structure):
+    _fields_ = [
+        ("stages", C.c_int32), ("n_nodes", C.c_int32), ("n_p", C.c_int32),
+        ("n_conv", C.c_int32), ("nnz", C.c_int32), ("dt", C.c_double),
+        ("butcher_a", C.c_double * (IVK_MAX_STAGES * IVK_MAX_STAGES)),
+        ("p2_rowptr", C.c_void_p), ("p2_col", C.c_void_p), ("p2_mk", C.c_void_p),
+        ("conv", C.c_void_p),
+        ("b_rowptr", C.c_void_p), ("b_col", C.c_void_p), ("b_val", C.c_void_p),
+        ("bt_rowptr", C.c_void_p), ("bt_col", C.c_void_p), ("bt_val", C.c_void_p),
+        ("node_constrained", C.c_void_p),
+    ]
+
+
+class PatchDesc(C.Structure):
+    _fields_ = [
+        ("num_patches", C.c_int32), ("dim", C.c_int32), ("max_m", C.c_int32),
+        ("total_m", C.c_int32),
+        ("idx_off", C.c_void_p), ("idx", C.c_void_p), ("inv_off", C.c_void_p),
+        ("inv", C.c_void_p), ("dof_ptr", C.c_void_p), ("dof_pos", C.c_void_p),
+        ("vertex", C.c_void_p), ("node_off", C.c_void_p), ("node", C.c_void_p),
+    ]
+
+
+class TransferDesc(C.Structure):
+    _fields_ = [
+        ("stages", C.c_int32), ("nf_nodes", C.c_int32), ("nf_p", C.c_int32),
+        ("nc_nodes", C.c_int32), ("nc_p", C.c_int32),
+        ("p2_rowptr", C.c_void_p), ("p2_col", C.c_void_p), ("p2_val", C.c_void_p),
+        ("p2t_rowptr", C.c_void_p), ("p2t_col", C.c_void_p), ("p2t_val", C.c_void_p),
+        ("p1_rowptr", C.c_void_p), ("p1_col", C.c_void_p), ("p1_val", C.c_void_p),
+        ("p1t_rowptr", C.c_void_p), ("p1t_col", C.c_void_p), ("p1t_val", C.c_void_p),
+        ("fine_constrained", C.c_void_p), ("coarse_constrained", C.c_void_p),
+    ]
+
+
+class CoarseDesc(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32), ("stages", C.c_int32), ("n_u", C.c_int32), ("n_p", C.c_int32),
+        ("lower", C.c_void_p), ("upper", C.c_void_p),
+        ("perm_r", C.c_void_p), ("perm_c", C.c_void_p),
+    ]
+
+
+# name -> argtypes (restype int unless noted)
+_P = C.c_void_p
+_SIGS = {
+    "ivk_last_error": ([], C.c_char_p),
+    "ivk_version": ([], C.c_int),
+    "ivk_launch_count": ([], C.c_int64),
+    "ivk_stage_apply": ([C.POINTER(OperatorDesc), _P, _P, _P, _P], C.c_int),
+    "ivk_patch_apply": ([C.POINTER(PatchDesc), _P, _P, _P], C.c_int),
+    "ivk_patch_combine": ([C.POINTER(PatchDesc), _P, _P, C.c_double, C.c_double, _P, _P, _P, _P],
+                          C.c_int),
+    "ivk_patch_factor": ([C.POINTER(OperatorDesc), C.POINTER(PatchDesc), _P, _P], C.c_int),
+    "ivk_vanka_sweep": ([C.POINTER(OperatorDesc), C.POINTER(PatchDesc), _P, _P, C.c_double, _P,
+                         _P, _P, _P, _P], C.c_int),
+    "ivk_restrict": ([C.POINTER(TransferDesc), _P, _P, _P], C.c_int),
+    "ivk_prolong_add": ([C.POINTER(TransferDesc), _P, _P, _P], C.c_int),
+    "ivk_coarse_solve": ([C.POINTER(CoarseDesc), _P, _P, _P], C.c_int),
+    "ivk_project_pressure_means": ([C.c_int32, C.c_int32, C.c_int32, _P, _P], C.c_int),
+    "ivk_axpby": ([C.c_int64, C.c_double, _P, C.c_double, _P, _P, _P], C.c_int),
+    "ivk_seed_constrained": ([C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P], C.c_int),
+}
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load(path=_LIB_PATH):
+    """Load libivk.so (raises if it is absent -- no fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise IvkError(
+            f"libivk.so not found at {path}; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+    lib = C.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def lib():
+    return load()
+
+
+def check(rc, what=""):
+    if rc == 0:
+        return
+    msg = load().ivk_last_error().decode(errors="replace")
+    if rc == IVK_ESINGULAR:
+        raise SingularPatch(f"{what}: {msg}")
+    raise IvkError(f"{what} failed ({rc}): {msg}")

@@ -1,0 +1,410 @@
+// K2-K4 and K7: the vertex-star Vanka patch set on sm_100a, fp64.
+//
+//  K2+K3 ivk_patch_apply   gather r at each patch's DoFs and apply the stored
+//                          dense inverse (solvers.py:218-220).  HBM-bound: the
+//                          inverse store is streamed exactly once per sweep
+//                          with 256-bit evict-first loads; r stays in L2.
+//  K4    ivk_patch_combine deterministic owner-computes scatter-add
+//                          (np.bincount, solvers.py:221) fused with the sweep
+//                          update x + omega * W * z (solvers.py:239).
+//  K7    ivk_patch_factor  assemble each stage-coupled patch matrix from the
+//                          scalar operator (solvers.py:186-212) and invert it
+//                          by Gauss-Jordan with partial pivoting in shared
+//                          memory (replaces np.linalg.inv, solvers.py:177).
+
+#include <climits>
+
+#include "ivk_common.cuh"
+
+namespace ivk {
+
+int validate_op(const ivk_operator_desc* d);  // ivk_operator.cu
+
+struct PatchParams {
+  int num_patches, dim, max_m, total_m;
+  const int32_t* __restrict__ idx_off;
+  const int32_t* __restrict__ idx;
+  const int64_t* __restrict__ inv_off;
+  double* inv;
+  const int32_t* __restrict__ dof_ptr;
+  const int32_t* __restrict__ dof_pos;
+  const int32_t* __restrict__ vertex;
+  const int32_t* __restrict__ node_off;
+  const int32_t* __restrict__ node;
+};
+
+static PatchParams make_patch_params(const ivk_patch_desc* d) {
+  PatchParams p;
+  p.num_patches = d->num_patches;
+  p.dim = d->dim;
+  p.max_m = d->max_m;
+  p.total_m = d->total_m;
+  p.idx_off = d->idx_off;
+  p.idx = d->idx;
+  p.inv_off = d->inv_off;
+  p.inv = d->inv;
+  p.dof_ptr = d->dof_ptr;
+  p.dof_pos = d->dof_pos;
+  p.vertex = d->vertex;
+  p.node_off = d->node_off;
+  p.node = d->node;
+  return p;
+}
+
+static int validate_patches(const ivk_patch_desc* d) {
+  IVK_REQUIRE(d != nullptr, "patch descriptor is NULL");
+  IVK_REQUIRE(d->num_patches > 0 && d->dim > 0 && d->max_m > 0, "empty patch set");
+  IVK_REQUIRE(d->idx_off && d->idx && d->inv_off && d->inv && d->dof_ptr && d->dof_pos,
+              "patch descriptor has a NULL array");
+  return IVK_OK;
+}
+
+// ------------------------------------------------------------------ K2+K3
+//
+// One warp per patch.  Lane t owns output rows 4t..4t+3 of a 128-row chunk;
+// for each column j it issues one 256-bit streaming load of Inv^T[j][4t..4t+3]
+// (a warp reads 1 KB contiguous per j) and broadcasts r_p[j] from shared
+// memory.  Patches wider than 128 loop over row chunks.
+constexpr int kApplyWarps = 8;
+constexpr int kRowsPerWarp = 128;
+constexpr int kUnroll = 4;  // 4 x 32 B in flight per lane; ~48 regs -> 40 warps/SM
+
+__device__ __forceinline__ void ld_stream4(const double* p, double& a, double& b, double& c,
+                                           double& d) {
+  asm volatile("ld.global.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
+
+template <int MAXM>
+__global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kernel(PatchParams pd,
+                                                                       const double* __restrict__ r,
+                                                                       double* __restrict__ local) {
+  __shared__ __align__(16) double rs_all[kApplyWarps][MAXM];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* rs = rs_all[warp];
+  const int stride = gridDim.x * kApplyWarps;
+  for (int p = blockIdx.x * kApplyWarps + warp; p < pd.num_patches; p += stride) {
+    const int off = pd.idx_off[p];
+    const int m = pd.idx_off[p + 1] - off;
+    const int ld = (m + 3) & ~3;
+    for (int j = lane; j < m; j += 32) rs[j] = __ldg(r + pd.idx[off + j]);
+    __syncwarp();
+    const double* inv = pd.inv + pd.inv_off[p];
+    for (int row0 = 0; row0 < m; row0 += kRowsPerWarp) {
+      const int i0 = row0 + 4 * lane;
+      if (i0 < ld) {
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+        const double* col = inv + i0;
+        int j = 0;
+#pragma unroll 1
+        for (; j + kUnroll <= m; j += kUnroll) {
+          double v[kUnroll][4];
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u)
+            ld_stream4(col + (long)(j + u) * ld, v[u][0], v[u][1], v[u][2], v[u][3]);
+#pragma unroll
+          for (int u = 0; u < kUnroll; ++u) {
+            const double rj = rs[j + u];
+            acc0 = fma(v[u][0], rj, acc0);
+            acc1 = fma(v[u][1], rj, acc1);
+            acc2 = fma(v[u][2], rj, acc2);
+            acc3 = fma(v[u][3], rj, acc3);
+          }
+        }
+        for (; j < m; ++j) {
+          double v0, v1, v2, v3;
+          ld_stream4(col + (long)j * ld, v0, v1, v2, v3);
+          const double rj = rs[j];
+          acc0 = fma(v0, rj, acc0);
+          acc1 = fma(v1, rj, acc1);
+          acc2 = fma(v2, rj, acc2);
+          acc3 = fma(v3, rj, acc3);
+        }
+        double* out = local + off + i0;
+        if (i0 + 0 < m) out[0] = acc0;
+        if (i0 + 1 < m) out[1] = acc1;
+        if (i0 + 2 < m) out[2] = acc2;
+        if (i0 + 3 < m) out[3] = acc3;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// -------------------------------------------------------------------- K4
+
+__global__ void patch_combine_kernel(PatchParams pd, const double* __restrict__ local,
+                                     const double* x, double alpha, double beta,
+                                     const double* __restrict__ w, double* out, double* accum) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < pd.dim; d += gridDim.x * blockDim.x) {
+    const int k0 = pd.dof_ptr[d], k1 = pd.dof_ptr[d + 1];
+    double z = 0.0;
+    for (int k = k0; k < k1; ++k) z += local[pd.dof_pos[k]];
+    double v = beta * (w ? w[d] : 1.0) * z;
+    if (x) v = alpha * x[d] + v;
+    out[d] = v;
+    if (accum) accum[d] += v;
+  }
+}
+
+// -------------------------------------------------------------------- K7
+
+struct FactorParams {
+  int n_nodes, n_p, n_conv, nnz, S;
+  double dt;
+  double a[IVK_MAX_STAGES * IVK_MAX_STAGES];
+  const int32_t* __restrict__ p2_rowptr;
+  const int32_t* __restrict__ p2_col;
+  const double2* __restrict__ p2_mk;
+  const double4* __restrict__ conv;
+  const int32_t* __restrict__ b_rowptr;
+  const int32_t* __restrict__ b_col;
+  const double2* __restrict__ b_val;
+};
+
+// Position of `col` in the sorted CSR row [lo, hi), or -1.
+__device__ __forceinline__ int find_col(const int32_t* __restrict__ cols, int lo, int hi, int col) {
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const int c = cols[mid];
+    if (c == col) return mid;
+    if (c < col) lo = mid + 1; else hi = mid;
+  }
+  return -1;
+}
+
+constexpr int kFactorThreads = 512;
+
+// One CTA per patch; the d x d matrix lives in dynamic shared memory
+// (row-major, leading dimension d).  Local layout (solvers.py:160-165,
+// 196-211): stage block a occupies rows a*(mv+1) .. a*(mv+1)+mv, velocity
+// DoFs 2*alpha + c for the patch's free nodes, then the vertex pressure.
+__global__ void __launch_bounds__(kFactorThreads) patch_factor_kernel(FactorParams op, PatchParams pd,
+                                                                      int32_t* singular) {
+  extern __shared__ __align__(16) double A[];
+  __shared__ int piv[512];
+  __shared__ double colk[512];
+  __shared__ int s_prow;
+  __shared__ int s_bad;
+  const int p = blockIdx.x;
+  const int S = op.S;
+  const int n0 = pd.node_off[p], nk = pd.node_off[p + 1] - n0;
+  const int* nodes = pd.node + n0;
+  const int v = pd.vertex[p];
+  const int mv = 2 * nk, blk = mv + 1, d = S * blk;
+  const int tid = threadIdx.x;
+
+  for (int e = tid; e < d * d; e += blockDim.x) A[e] = 0.0;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+
+  // Velocity-velocity blocks: M delta_ab + dt a_ab (K + J_a).
+  for (int pr = tid; pr < nk * nk; pr += blockDim.x) {
+    const int al = pr / nk, be = pr % nk;
+    const int row = nodes[al];
+    const int pos = find_col(op.p2_col, op.p2_rowptr[row], op.p2_rowptr[row + 1], nodes[be]);
+    if (pos < 0) continue;  // not coupled: zero block
+    const double2 mk = op.p2_mk[pos];
+    for (int a = 0; a < S; ++a) {
+      double4 J = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (op.n_conv == 1) J = op.conv[pos];
+      else if (op.n_conv > 1) J = op.conv[(long)a * op.nnz + pos];
+      for (int b = 0; b < S; ++b) {
+        const double f = op.dt * op.a[a * S + b];
+        const double diag = (a == b ? mk.x : 0.0) + f * mk.y;
+        double* base = A + (long)(a * blk + 2 * al) * d + b * blk + 2 * be;
+        base[0] = diag + f * J.x;
+        base[1] = f * J.y;
+        base[d] = f * J.z;
+        base[d + 1] = diag + f * J.w;
+      }
+    }
+  }
+  // Velocity-pressure couplings with the patch vertex: dt a_ab B[vel, v].
+  for (int al = tid; al < nk; al += blockDim.x) {
+    const int row = nodes[al];
+    const int pos = find_col(op.b_col, op.b_rowptr[row], op.b_rowptr[row + 1], v);
+    const double2 bv = pos >= 0 ? op.b_val[pos] : make_double2(0.0, 0.0);
+    for (int a = 0; a < S; ++a)
+      for (int b = 0; b < S; ++b) {
+        const double f = op.dt * op.a[a * S + b];
+        const int r0 = a * blk + 2 * al, c0 = b * blk + 2 * al;
+        A[(long)r0 * d + b * blk + mv] = f * bv.x;
+        A[(long)(r0 + 1) * d + b * blk + mv] = f * bv.y;
+        A[(long)(a * blk + mv) * d + c0] = f * bv.x;
+        A[(long)(a * blk + mv) * d + c0 + 1] = f * bv.y;
+      }
+  }
+  __syncthreads();
+
+  // In-place Gauss-Jordan inverse with row pivoting (first max |pivot|, as
+  // LAPACK idamax); columns are unscrambled at the end.
+  for (int k = 0; k < d; ++k) {
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + tid; i < d; i += 32) {
+        const double a = fabs(A[(long)i * d + k]);
+        if (a > best) { best = a; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_down_sync(0xffffffffu, best, o);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tid == 0) {
+        s_prow = bi;
+        piv[k] = bi;
+        if (!(best > 0.0)) s_bad = 1;
+      }
+    }
+    __syncthreads();
+    if (s_bad) break;
+    const int pr = s_prow;
+    if (pr != k) {
+      for (int j = tid; j < d; j += blockDim.x) {
+        const double t = A[(long)k * d + j];
+        A[(long)k * d + j] = A[(long)pr * d + j];
+        A[(long)pr * d + j] = t;
+      }
+      __syncthreads();
+    }
+    const double pinv = 1.0 / A[(long)k * d + k];
+    for (int i = tid; i < d; i += blockDim.x) colk[i] = (i == k) ? 0.0 : A[(long)i * d + k];
+    __syncthreads();
+    for (int j = tid; j < d; j += blockDim.x)
+      A[(long)k * d + j] = (j == k) ? pinv : A[(long)k * d + j] * pinv;
+    __syncthreads();
+    for (int e = tid; e < d * d; e += blockDim.x) {
+      const int i = e / d, j = e - i * d;
+      if (i == k) continue;
+      const double f = colk[i];
+      const double base = (j == k) ? 0.0 : A[e];
+      A[e] = base - f * A[(long)k * d + j];
+    }
+    __syncthreads();
+  }
+  if (s_bad) {
+    if (tid == 0) atomicMin(singular, v);
+    return;
+  }
+  for (int k = d - 1; k >= 0; --k) {
+    const int pk = piv[k];
+    if (pk != k) {
+      for (int i = tid; i < d; i += blockDim.x) {
+        const double t = A[(long)i * d + k];
+        A[(long)i * d + k] = A[(long)i * d + pk];
+        A[(long)i * d + pk] = t;
+      }
+      __syncthreads();
+    }
+  }
+  // Store Inv^T with leading dimension ld: inv[j*ld + i] = Inv[i][j].
+  const int ld = (d + 3) & ~3;
+  double* out = pd.inv + pd.inv_off[p];
+  for (int e = tid; e < d * ld; e += blockDim.x) {
+    const int j = e / ld, i = e - j * ld;
+    out[e] = (i < d) ? A[(long)i * d + j] : 0.0;
+  }
+}
+
+}  // namespace ivk
+
+using namespace ivk;
+
+extern "C" {
+
+int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, void* stream) {
+  int rc = validate_patches(pd);
+  if (rc) return rc;
+  IVK_REQUIRE(r && local, "r/local is NULL");
+  PatchParams p = make_patch_params(pd);
+  const int blocks_needed = (pd->num_patches + kApplyWarps - 1) / kApplyWarps;
+  int grid = blocks_needed;
+  const int cap = kSMs * 8;  // persistent-ish: 8 CTAs (64 warps) per SM
+  if (grid > cap) grid = cap;
+  cudaStream_t st = as_stream(stream);
+  if (pd->max_m <= 128)
+    patch_apply_kernel<128><<<grid, kApplyWarps * 32, 0, st>>>(p, r, local);
+  else if (pd->max_m <= 256)
+    patch_apply_kernel<256><<<grid, kApplyWarps * 32, 0, st>>>(p, r, local);
+  else if (pd->max_m <= 512)
+    patch_apply_kernel<512><<<grid, kApplyWarps * 32, 0, st>>>(p, r, local);
+  else {
+    set_error("ivk_patch_apply: patch size %d > 512 unsupported", pd->max_m);
+    return IVK_EUNSUPPORTED;
+  }
+  return check_launch("ivk_patch_apply");
+}
+
+int ivk_patch_combine(const ivk_patch_desc* pd, const double* local, const double* x, double alpha,
+                      double beta, const double* w, double* out, double* accum, void* stream) {
+  int rc = validate_patches(pd);
+  if (rc) return rc;
+  IVK_REQUIRE(local && out, "local/out is NULL");
+  PatchParams p = make_patch_params(pd);
+  int grid = (pd->dim + 255) / 256;
+  if (grid > kSMs * 16) grid = kSMs * 16;
+  patch_combine_kernel<<<grid, 256, 0, as_stream(stream)>>>(p, local, x, alpha, beta, w, out, accum);
+  return check_launch("ivk_patch_combine");
+}
+
+int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int32_t* singular_dev,
+                     void* stream) {
+  int rc = validate_op(op);
+  if (rc) return rc;
+  rc = validate_patches(pd);
+  if (rc) return rc;
+  IVK_REQUIRE(pd->vertex && pd->node_off && pd->node && singular_dev,
+              "patch factorisation needs vertex/node tables and a singular flag");
+  const int dmax = pd->max_m;
+  if (dmax > 512) {
+    set_error("ivk_patch_factor: patch size %d > 512 unsupported", dmax);
+    return IVK_EUNSUPPORTED;
+  }
+  const size_t smem = (size_t)dmax * dmax * sizeof(double);
+  if (smem > 220 * 1024) {
+    set_error("ivk_patch_factor: patch size %d needs %zu B shared memory", dmax, smem);
+    return IVK_EUNSUPPORTED;
+  }
+  cudaError_t e = cudaFuncSetAttribute(patch_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) {
+    set_error("ivk_patch_factor: %s", cudaGetErrorString(e));
+    return IVK_ECUDA;
+  }
+  FactorParams f;
+  f.n_nodes = op->n_nodes;
+  f.n_p = op->n_p;
+  f.n_conv = op->n_conv;
+  f.nnz = op->nnz;
+  f.S = op->stages;
+  f.dt = op->dt;
+  for (int i = 0; i < IVK_MAX_STAGES * IVK_MAX_STAGES; ++i) f.a[i] = op->butcher_a[i];
+  f.p2_rowptr = op->p2_rowptr;
+  f.p2_col = op->p2_col;
+  f.p2_mk = reinterpret_cast<const double2*>(op->p2_mk);
+  f.conv = reinterpret_cast<const double4*>(op->conv);
+  f.b_rowptr = op->b_rowptr;
+  f.b_col = op->b_col;
+  f.b_val = reinterpret_cast<const double2*>(op->b_val);
+  PatchParams p = make_patch_params(pd);
+  patch_factor_kernel<<<pd->num_patches, kFactorThreads, smem, as_stream(stream)>>>(f, p,
+                                                                                    singular_dev);
+  return check_launch("ivk_patch_factor");
+}
+
+int ivk_vanka_sweep(const ivk_operator_desc* op, const ivk_patch_desc* pd, const double* x,
+                    const double* b, double omega, const double* w, double* r, double* local,
+                    double* x_out, void* stream) {
+  IVK_REQUIRE(x && b && r && local && x_out, "sweep vector is NULL");
+  int rc = ivk_stage_apply(op, x, b, r, stream);
+  if (rc) return rc;
+  rc = ivk_patch_apply(pd, r, local, stream);
+  if (rc) return rc;
+  return ivk_patch_combine(pd, local, x, 1.0, omega, w, x_out, nullptr, stream);
+}
+
+}  // extern "C"

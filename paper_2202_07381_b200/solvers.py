@@ -1,0 +1,679 @@
+"""Monolithic multigrid with additive IRK-Vanka relaxation -- the hot path.
+
+Host mirror of the reference ``irkmg.solvers`` API
+(/root/reference/pkg/src/irkmg/solvers.py); every flop of the relaxation,
+the transfers and the coarse solve runs in libivk (sm_100a):
+
+    reference                         here                       kernel
+    StageSystem.matvec / b - A x      StageSystem.apply_into     K1
+    resid[idx] + einsum               VankaPatchSet._apply       K2+K3
+    np.bincount + x + w z             VankaPatchSet._combine     K4
+    np.linalg.inv (setup)             ivk_patch_factor           K7
+    P.T @ r / P @ e                   StageTransfer              K5
+    CoarseSolver.solve (splu)         CoarseSolver.solve         K6
+    chebyshev recurrence, projections ivk_patch_combine/axpby    K8
+
+Numpy inputs are accepted at the public edge (copied to and from the
+device); CUDA tensors stay resident.  There is no CPU fallback.
+"""
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from . import _lib
+from .patches import build_patch_tables
+
+__all__ = [
+    "PatchSingularError",
+    "SmootherSpec",
+    "KrylovStats",
+    "VankaPatchSet",
+    "build_vanka_patches",
+    "apply_vanka",
+    "chebyshev_smooth",
+    "CoarseSolver",
+    "coarse_direct_solve",
+    "MGLevel",
+    "MGHierarchyOp",
+    "vcycle",
+    "fgmres",
+]
+
+
+class PatchSingularError(RuntimeError):
+    """Singular Vanka patch matrix (solvers.py:81-84)."""
+
+    def __init__(self, vertex):
+        super().__init__(f"singular Vanka patch matrix at vertex {vertex}")
+        self.vertex = vertex
+
+
+@dataclass
+class SmootherSpec:
+    """Relaxation configuration (solvers.py:87-105), extended with the
+    stationary ``"richardson"`` driver and partition-of-unity weighting used
+    by the BASELINE "damping 0.5" smoother."""
+
+    pre: int = 2
+    post: int = 2
+    accel: str = "chebyshev"  # "chebyshev" | "gmres" | "richardson"
+    cheby_a: float = 2.0
+    cheby_b: float = 8.0
+    omega: float = 1.0
+    weighting: str = "none"   # "none" (reference) | "pou" (1 / multiplicity)
+
+    def __post_init__(self):
+        if self.accel not in ("chebyshev", "gmres", "richardson"):
+            raise ValueError(f"unknown smoother acceleration {self.accel!r}")
+        if self.accel == "chebyshev" and not 0.0 < self.cheby_a < self.cheby_b:
+            raise ValueError("Chebyshev interval must satisfy 0 < a < b")
+        if min(self.pre, self.post) < 0:
+            raise ValueError("sweep counts must be >= 0")
+        if self.weighting not in ("none", "pou"):
+            raise ValueError(f"unknown weighting {self.weighting!r}")
+
+
+@dataclass
+class KrylovStats:
+    iterations: int = 0
+    residual_norms: list = field(default_factory=list)
+    final_residual: float = np.inf
+    relative_residual: float = np.inf
+    converged: bool = False
+
+
+# ----------------------------------------------------------------- patches
+
+class VankaPatchSet:
+    """Vertex-star patches with device-resident dense inverses (solvers.py:116-222).
+
+    One patch per mesh vertex: every unconstrained velocity DoF (both
+    components, all stages) on the closure of the vertex star plus the r
+    centre pressures.  Inverses are assembled and factorised on the GPU
+    (K7) unless ``factor=False`` (then ``set_inverses`` must be called).
+    """
+
+    def __init__(self, system, mesh, omega=1.0, factor=True):
+        self.omega = float(omega)
+        self.system = system
+        self.num_patches = mesh.num_vertices
+        self.tables = build_patch_tables(mesh, system.n_nodes, system.n_p, system.r,
+                                         system.node_constrained)
+        self._dev = None
+        self._factored = False
+        if factor:
+            self.factor()
+
+    # -- reference attributes ------------------------------------------------
+
+    @property
+    def patch_indices(self):
+        """Per-vertex stage-major index arrays (solvers.py:160-166)."""
+        t = self.tables
+        out = [None] * t.num_patches
+        for k, v in enumerate(t.order):
+            out[v] = t.idx[t.idx_off[k]:t.idx_off[k + 1]].copy()
+        return out
+
+    @property
+    def patch_vel(self):
+        t = self.tables
+        out = [None] * t.num_patches
+        for k, v in enumerate(t.order):
+            n = t.node[t.node_off[k]:t.node_off[k + 1]]
+            vel = np.empty(2 * len(n), dtype=np.int64)
+            vel[0::2] = 2 * n
+            vel[1::2] = 2 * n + 1
+            out[v] = vel
+        return out
+
+    @property
+    def groups(self):
+        """[(idx (P, m), inv (P, m, m))] in the reference group order,
+        downloaded from the device (solvers.py:169-184)."""
+        t = self.tables
+        dev = self.device_data()
+        inv_all = dev["inv"]
+        out = []
+        for m, first, count in t.groups():
+            ld = (m + 3) & ~3
+            off = int(t.inv_off[first])
+            blk = inv_all[off:off + count * m * ld].view(count, m, ld)[:, :, :m]
+            inv = blk.transpose(1, 2).contiguous().cpu().numpy()
+            idx = t.idx[t.idx_off[first]:t.idx_off[first + count]].reshape(count, m)
+            out.append((idx.copy(), inv))
+        return out
+
+    @property
+    def multiplicity(self):
+        return self.tables.multiplicity
+
+    def pou_weights(self):
+        """W = 1 / multiplicity (0 where no patch covers the DoF)."""
+        mult = self.tables.multiplicity
+        w = np.zeros(len(mult))
+        nz = mult > 0
+        w[nz] = 1.0 / mult[nz]
+        return w
+
+    # -- device data ---------------------------------------------------------
+
+    def device_data(self):
+        if self._dev is not None:
+            return self._dev
+        from ._device import upload
+        import torch
+        t = self.tables
+        if t.total_m >= 2 ** 31:
+            raise ValueError("patch index total exceeds int32")
+        d = {}
+        d["idx_off"] = upload(t.idx_off, np.int32)
+        d["idx"] = upload(t.idx, np.int32)
+        d["inv_off"] = upload(t.inv_off, np.int64)
+        d["inv"] = torch.zeros(t.inv_size, dtype=torch.float64, device=d["idx"].device)
+        d["dof_ptr"] = upload(t.dof_ptr, np.int32)
+        d["dof_pos"] = upload(t.dof_pos, np.int32)
+        d["vertex"] = upload(t.order, np.int32)
+        d["node_off"] = upload(t.node_off, np.int32)
+        d["node"] = upload(t.node, np.int32)
+        d["local"] = torch.empty(t.total_m, dtype=torch.float64, device=d["idx"].device)
+        d["pou"] = upload(self.pou_weights(), np.float64)
+        desc = _lib.PatchDesc()
+        desc.num_patches = t.num_patches
+        desc.dim = t.dim
+        desc.max_m = t.max_m
+        desc.total_m = t.total_m
+        for name in ("idx_off", "idx", "inv_off", "inv", "dof_ptr", "dof_pos", "vertex",
+                     "node_off", "node"):
+            setattr(desc, name, d[name].data_ptr())
+        d["desc"] = desc
+        self._dev = d
+        return d
+
+    @property
+    def desc(self):
+        return self.device_data()["desc"]
+
+    def factor(self):
+        """K7: assemble + invert every patch matrix on the GPU."""
+        import torch
+        from ._device import ptr, stream
+        dev = self.device_data()
+        flag = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev["idx"].device)
+        _lib.check(_lib.lib().ivk_patch_factor(self.system.desc, dev["desc"], ptr(flag), stream()),
+                   "patch_factor")
+        bad = int(flag.item())
+        if bad != 2 ** 31 - 1:
+            raise PatchSingularError(bad)
+        self._factored = True
+
+    def set_inverses(self, groups):
+        """Parity mode: install host inverses given in the reference ``groups``
+        format [(idx (P,m), inv (P,m,m))] instead of factorising on the GPU."""
+        import torch
+        t = self.tables
+        dev = self.device_data()
+        mine = t.groups()
+        if len(groups) != len(mine):
+            raise ValueError("group structure differs from this patch set")
+        for (m, first, count), (idx, inv) in zip(mine, groups):
+            idx = np.asarray(idx)
+            if idx.shape != (count, m) or not np.array_equal(
+                    idx.ravel(), t.idx[t.idx_off[first]:t.idx_off[first + count]]):
+                raise ValueError(f"patch indices of size group {m} differ")
+            ld = (m + 3) & ~3
+            blk = np.zeros((count, m, ld))
+            blk[:, :, :m] = np.transpose(np.asarray(inv, dtype=np.float64), (0, 2, 1))
+            off = int(t.inv_off[first])
+            dev["inv"][off:off + blk.size] = torch.from_numpy(blk.ravel()).to(dev["inv"].device)
+        self._factored = True
+
+    def _require(self):
+        if not self._factored:
+            raise RuntimeError("patch inverses are not available (call factor() or set_inverses())")
+
+    def apply_local(self, r, local=None):
+        """K2+K3 on device: local = blockdiag(Inv_p) gathered r."""
+        from ._device import ptr, stream
+        self._require()
+        dev = self.device_data()
+        local = dev["local"] if local is None else local
+        _lib.check(_lib.lib().ivk_patch_apply(dev["desc"], ptr(r), ptr(local), stream()),
+                   "patch_apply")
+        return local
+
+    def combine(self, local, x, alpha, beta, w, out, accum=None):
+        """K4 on device: out = alpha x + beta W sum_i R_i^T local_i (+ accum)."""
+        from ._device import ptr, stream
+        _lib.check(_lib.lib().ivk_patch_combine(self.desc, ptr(local), ptr(x), float(alpha),
+                                                float(beta), ptr(w), ptr(out), ptr(accum),
+                                                stream()), "patch_combine")
+        return out
+
+    def weights(self, weighting):
+        return None if weighting == "none" else self.device_data()["pou"]
+
+    def solve_additive(self, resid):
+        """z = sum_i R_i^T (R_i A R_i^T)^{-1} R_i resid (solvers.py:214-222)."""
+        from ._device import as_device_vector, to_host
+        import torch
+        rd, host = as_device_vector(resid, self.tables.dim)
+        z = torch.empty_like(rd)
+        loc = self.apply_local(rd)
+        self.combine(loc, None, 0.0, 1.0, None, z)
+        return to_host(z) if host else z
+
+
+def build_vanka_patches(system, mesh, omega=1.0):
+    """Vanka patch set for a stage system on ``mesh`` (solvers.py:225-229)."""
+    if system.n_p != mesh.num_vertices:
+        raise ValueError("mesh does not match the pressure space of the system")
+    return VankaPatchSet(system, mesh, omega=omega)
+
+
+def apply_vanka(patches, system, x, b, omega=None, weights=None):
+    """One additive Schwarz sweep x + omega W sum R_i^T A_i^-1 R_i (b - A x)
+    (solvers.py:232-239) as one fused K1 -> K3 -> K4 pass.
+
+    ``weights``: None (reference, unweighted), "pou", or a DoF vector."""
+    from ._device import as_device_vector, ptr, stream, to_host, upload
+    import torch
+    w = patches.omega if omega is None else omega
+    xd, host = as_device_vector(x, system.dim)
+    bd, _ = as_device_vector(b, system.dim)
+    if isinstance(weights, str):
+        wd = patches.weights(weights)
+    elif weights is None:
+        wd = None
+    else:
+        wd, _ = as_device_vector(weights, system.dim)
+    patches._require()
+    dev = patches.device_data()
+    r = torch.empty_like(xd)
+    out = torch.empty_like(xd)
+    _lib.check(_lib.lib().ivk_vanka_sweep(system.desc, dev["desc"], ptr(xd), ptr(bd), float(w),
+                                          ptr(wd), ptr(r), ptr(dev["local"]), ptr(out), stream()),
+               "vanka_sweep")
+    return to_host(out) if host else out
+
+
+def chebyshev_smooth(op_apply, precond, a, b, steps, x, rhs):
+    """Chebyshev-accelerated preconditioned Richardson (solvers.py:242-268).
+
+    Generic three-term recurrence over any array type (numpy or CUDA
+    tensors); the multigrid cycle uses a fused device version of it."""
+    if not 0.0 < a < b:
+        raise ValueError("Chebyshev interval must satisfy 0 < a < b")
+    if steps <= 0:
+        return x
+    theta = 0.5 * (b + a)
+    delta = 0.5 * (b - a)
+    sigma1 = theta / delta
+    rho = 1.0 / sigma1
+    x = x.clone() if hasattr(x, "clone") else x.copy()
+    r = rhs - op_apply(x)
+    z = precond(r)
+    d = z / theta
+    for _ in range(1, steps):
+        x += d
+        r = r - op_apply(d)
+        z = precond(r)
+        rho_new = 1.0 / (2.0 * sigma1 - rho)
+        d = rho_new * rho * d + (2.0 * rho_new / delta) * z
+        rho = rho_new
+    return x + d
+
+
+# ------------------------------------------------------------ coarse solve
+
+class CoarseSolver:
+    """Fixed SuperLU factorisation of A + Z Z^T (solvers.py:271-287).
+
+    The factorisation is the reference's own host setup (scipy ``splu`` with
+    its defaults); the per-cycle solve (projection, permuted dense
+    triangular solves, projection) is kernel K6 on the device."""
+
+    def __init__(self, system):
+        A = system.materialize()
+        Z = system.pressure_nullspace()
+        reg = sp.csr_matrix(Z @ Z.T)
+        self.lu = spla.splu((A + reg).tocsc())
+        self.Z = Z
+        self.system = system
+        self._dev = None
+
+    def device_data(self):
+        if self._dev is not None:
+            return self._dev
+        from ._device import upload
+        s = self.system
+        t = {
+            "lower": upload(self.lu.L.toarray(), np.float64),
+            "upper": upload(self.lu.U.toarray(), np.float64),
+            "perm_r": upload(self.lu.perm_r, np.int32),
+            "perm_c": upload(self.lu.perm_c, np.int32),
+        }
+        d = _lib.CoarseDesc()
+        d.n = s.dim
+        d.stages, d.n_u, d.n_p = s.r, s.n_u, s.n_p
+        for k in ("lower", "upper", "perm_r", "perm_c"):
+            setattr(d, k, t[k].data_ptr())
+        self._dev = {"tensors": t, "desc": d}
+        return self._dev
+
+    def solve_into(self, b, x):
+        from ._device import ptr, stream
+        _lib.check(_lib.lib().ivk_coarse_solve(self.device_data()["desc"], ptr(b), ptr(x),
+                                               stream()), "coarse_solve")
+        return x
+
+    def solve(self, b):
+        from ._device import as_device_vector, to_host
+        import torch
+        bd, host = as_device_vector(b, self.system.dim)
+        x = torch.empty_like(bd)
+        self.solve_into(bd, x)
+        return to_host(x) if host else x
+
+
+def coarse_direct_solve(system):
+    return CoarseSolver(system)
+
+
+# --------------------------------------------------------------- V-cycle
+
+@dataclass
+class MGLevel:
+    system: object
+    patches: Optional[VankaPatchSet]
+    smoother: SmootherSpec
+    prolong: Optional[object]  # StageTransfer from the next-coarser level
+
+
+class _LevelBuffers:
+    def __init__(self, dim, device):
+        import torch
+        self.x = torch.zeros(dim, dtype=torch.float64, device=device)
+        self.b = torch.zeros(dim, dtype=torch.float64, device=device)
+        self.r = torch.zeros(dim, dtype=torch.float64, device=device)
+        self.d = torch.zeros(dim, dtype=torch.float64, device=device)
+
+
+class MGHierarchyOp:
+    """V-cycle preconditioner over rediscretised levels (solvers.py:295-356).
+
+    ``levels`` runs coarsest to finest; ``levels[k].prolong`` maps level k-1
+    to level k.  The cycle runs entirely on the device on per-level scratch
+    buffers; ``precondition`` on a CUDA tensor can be captured once into a
+    CUDA graph (``use_graph=True``) and replayed.
+    """
+
+    def __init__(self, levels, coarse, use_graph=False):
+        self.levels = levels
+        self.coarse = coarse
+        for k, lev in enumerate(levels[1:], start=1):
+            if lev.prolong is None:
+                raise ValueError(f"level {k} is missing its prolongation")
+        self.use_graph = use_graph
+        self._bufs = None
+        self._graph = None
+
+    @property
+    def finest(self):
+        return self.levels[-1].system
+
+    def _buffers(self):
+        if self._bufs is None:
+            from ._device import device
+            dev = device()
+            self._bufs = [_LevelBuffers(lev.system.dim, dev) for lev in self.levels]
+            # Make sure every level's device data exists before any capture.
+            for lev in self.levels:
+                lev.system.device_data()
+                if lev.patches is not None and lev is not self.levels[0]:
+                    lev.patches.device_data()
+                if lev.prolong is not None:
+                    lev.prolong.device_data()
+            self.coarse.device_data()
+        return self._bufs
+
+    # -- smoothing (fused device versions of solvers.py:321-332) --------------
+
+    def _smooth(self, level, x, b, sweeps):
+        if sweeps == 0:
+            return
+        lev = self.levels[level]
+        sm = lev.smoother
+        sys_, pat = lev.system, lev.patches
+        buf = self._bufs[level]
+        w = pat.weights(sm.weighting)
+        if sm.accel == "richardson":
+            for _ in range(sweeps):
+                sys_.apply_into(x, b, buf.r)
+                loc = pat.apply_local(buf.r)
+                pat.combine(loc, x, 1.0, sm.omega, w, x)
+            return
+        if sm.accel == "chebyshev":
+            a, bb = sm.cheby_a, sm.cheby_b
+            theta = 0.5 * (bb + a)
+            delta = 0.5 * (bb - a)
+            sigma1 = theta / delta
+            rho = 1.0 / sigma1
+            sys_.apply_into(x, b, buf.r)
+            loc = pat.apply_local(buf.r)
+            pat.combine(loc, None, 0.0, sm.omega / theta, w, buf.d, accum=x)
+            for _ in range(1, sweeps):
+                sys_.apply_into(buf.d, buf.r, buf.r)
+                loc = pat.apply_local(buf.r)
+                rho_new = 1.0 / (2.0 * sigma1 - rho)
+                pat.combine(loc, buf.d, rho_new * rho, 2.0 * rho_new / delta * sm.omega, w,
+                            buf.d, accum=x)
+                rho = rho_new
+            return
+        # GMRES-accelerated smoothing: inner FGMRES, fixed sweep count.
+        import torch
+
+        def precond(v):
+            z = torch.empty_like(v)
+            loc = pat.apply_local(v)
+            pat.combine(loc, None, 0.0, sm.omega, w, z)
+            return z
+
+        xs, _ = fgmres(sys_.matvec, b, precond=precond, x0=x, rtol=0.0, atol=0.0,
+                       maxiter=sweeps, restart=sweeps)
+        x.copy_(xs)
+
+    def _cycle(self, level, x, b):
+        """In place: x <- V-cycle(level, x, b) (solvers.py:334-347)."""
+        if level == 0:
+            self.coarse.solve_into(b, x)
+            return
+        lev = self.levels[level]
+        buf = self._bufs[level]
+        below = self._bufs[level - 1]
+        self._smooth(level, x, b, lev.smoother.pre)
+        lev.system.apply_into(x, b, buf.r)
+        lev.prolong.restrict_into(buf.r, below.b)
+        below.x.zero_()
+        self._cycle(level - 1, below.x, below.b)
+        lev.prolong.prolong_add(below.x, x)
+        self._smooth(level, x, b, lev.smoother.post)
+
+    # -- public API ----------------------------------------------------------
+
+    def vcycle(self, level, x, b):
+        """One V-cycle at ``level`` (returns a new array, solvers.py:334)."""
+        from ._device import as_device_vector, to_host
+        self._buffers()
+        dim = self.levels[level].system.dim
+        xd, host = as_device_vector(x, dim)
+        bd, _ = as_device_vector(b, dim)
+        out = xd.clone()
+        self._cycle(level, out, bd)
+        return to_host(out) if host else out
+
+    def precondition_into(self, r, z):
+        """Device: z = precondition(r) (solvers.py:349-356)."""
+        from ._device import ptr, stream
+        sys_ = self.finest
+        dev = sys_.device_data()
+        _lib.check(_lib.lib().ivk_seed_constrained(sys_.r, sys_.n_nodes, sys_.n_p,
+                                                   ptr(dev["tensors"]["cmask"]), ptr(r), ptr(z),
+                                                   stream()), "seed_constrained")
+        self._cycle(len(self.levels) - 1, z, r)
+        sys_.project_pressure_means(z)
+        return z
+
+    def _graph_precondition(self, r):
+        import torch
+        if self._graph is None:
+            self._g_in = torch.zeros_like(r)
+            self._g_out = torch.zeros_like(r)
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self.precondition_into(self._g_in, self._g_out)  # warm-up (attributes, caches)
+            torch.cuda.current_stream().wait_stream(s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.precondition_into(self._g_in, self._g_out)
+            self._graph = g
+        self._g_in.copy_(r)
+        self._graph.replay()
+        return self._g_out.clone()
+
+    def precondition(self, r):
+        """Preconditioner application for FGMRES: approximately solve A z = r."""
+        from ._device import as_device_vector, to_host
+        import torch
+        self._buffers()
+        rd, host = as_device_vector(r, self.finest.dim)
+        if self.use_graph and all(l.smoother.accel != "gmres" for l in self.levels[1:]):
+            z = self._graph_precondition(rd)
+        else:
+            z = torch.empty_like(rd)
+            self.precondition_into(rd, z)
+        return to_host(z) if host else z
+
+
+def vcycle(hierarchy, level, x, b):
+    """Module-level alias (solvers.py:359-361)."""
+    return hierarchy.vcycle(level, x, b)
+
+
+# ----------------------------------------------------------------- FGMRES
+
+def _is_torch(v):
+    try:
+        import torch
+        return isinstance(v, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        return False
+
+
+def fgmres(op_apply, b, precond=None, x0=None, rtol=1e-8, atol=0.0, maxiter=100, restart=30):
+    """Flexible right-preconditioned GMRES (solvers.py:364-443).
+
+    Same algorithm as the reference (MGS Arnoldi, Givens rotations, restart,
+    true-residual check at each cycle end, monotone reported envelope).
+    Runs on the device when ``b`` is a CUDA tensor (the small Hessenberg
+    least-squares problem stays on the host); numpy ``b`` runs on the host.
+    """
+    if _is_torch(b):
+        import torch
+        dev_ = b.device
+        n = b.numel()
+        x = torch.zeros(n, dtype=torch.float64, device=dev_) if x0 is None else \
+            torch.as_tensor(x0, dtype=torch.float64, device=dev_).clone()
+        norm = lambda v: float(torch.linalg.vector_norm(v))
+        zeros = lambda *s: torch.zeros(*s, dtype=torch.float64, device=dev_)
+        as_vec = lambda v: torch.as_tensor(v, dtype=torch.float64, device=dev_)
+        dot = torch.dot
+    else:
+        n = len(b)
+        x = np.zeros(n) if x0 is None else np.asarray(x0, dtype=float).copy()
+        norm = lambda v: float(np.linalg.norm(v))
+        zeros = lambda *s: np.zeros(s)
+        as_vec = lambda v: np.array(v, dtype=float)
+        dot = lambda u, v: u @ v
+    if precond is None:
+        precond = lambda v: v
+    stats = KrylovStats()
+
+    r = b - op_apply(x)
+    norm0 = norm(r)
+    stats.residual_norms.append(norm0)
+    tol = max(rtol * norm0, atol)
+    if norm0 <= tol:
+        stats.final_residual = norm0
+        stats.relative_residual = 0.0 if norm0 == 0 else 1.0
+        stats.converged = True
+        return x, stats
+
+    while stats.iterations < maxiter:
+        m = min(restart, maxiter - stats.iterations)
+        V = zeros(m + 1, n)
+        Z = zeros(m, n)
+        H = np.zeros((m + 1, m))
+        cs = np.zeros(m)
+        sn = np.zeros(m)
+        g = np.zeros(m + 1)
+
+        beta = norm(r)
+        V[0] = r / beta
+        g[0] = beta
+        k = 0
+        for j in range(m):
+            Z[j] = precond(V[j])
+            w = as_vec(op_apply(Z[j]))
+            if _is_torch(w):
+                w = w.clone()
+                hc = zeros(j + 1)
+                for i in range(j + 1):
+                    hc[i] = dot(w, V[i])
+                    w -= hc[i] * V[i]
+                H[:j + 1, j] = hc.cpu().numpy()
+            else:
+                for i in range(j + 1):
+                    H[i, j] = w @ V[i]
+                    w -= H[i, j] * V[i]
+            H[j + 1, j] = norm(w)
+            if H[j + 1, j] > 1e-300:
+                V[j + 1] = w / H[j + 1, j]
+            for i in range(j):
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            denom = np.hypot(H[j, j], H[j + 1, j])
+            cs[j] = H[j, j] / denom
+            sn[j] = H[j + 1, j] / denom
+            H[j, j] = denom
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            k = j + 1
+            stats.iterations += 1
+            est = abs(g[j + 1])
+            stats.residual_norms.append(est)
+            if est <= tol or stats.iterations >= maxiter:
+                break
+        y = np.linalg.solve(np.triu(H[:k, :k]), g[:k])
+        if _is_torch(x):
+            x = x + as_vec(y) @ Z[:k]
+        else:
+            x = x + y @ Z[:k]
+        r = b - op_apply(x)
+        true_norm = norm(r)
+        stats.residual_norms[-1] = true_norm
+        if true_norm <= tol:
+            break
+
+    stats.final_residual = norm(b - op_apply(x))
+    stats.relative_residual = stats.final_residual / norm0 if norm0 > 0 else 0.0
+    stats.converged = stats.final_residual <= tol
+    stats.residual_norms = list(np.minimum.accumulate(stats.residual_norms))
+    return x, stats

@@ -1,0 +1,292 @@
+"""The stage-coupled saddle-point operator (host mirror of the reference
+``StageSystem``, /root/reference/pkg/src/irkmg/stages.py:47-186).
+
+    [ I_s (x) diag(M, 0)  +  dt A (x) [[K, B], [B^T, 0]] ] k = F
+
+Vectors are stage-major ``[(u_1, p_1), ..., (u_s, p_s)]``.  The operator
+apply (``matvec``) and the residual run in libivk (kernel K1); this class
+owns the eliminated scalar-node data on the device and keeps the
+reference's layout helpers on the host.
+"""
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from .fem import ConvectionBlocks, StokesBlocks
+
+__all__ = ["StageSystem", "assemble_stage_operator"]
+
+
+class StageSystem:
+    """Drop-in for the reference ``StageSystem`` (stages.py:47-88).
+
+    Parameters
+    ----------
+    blocks : StokesBlocks
+        Raw (non-eliminated) scalar-node M, K, B.
+    tableau : ButcherTableau (needs ``.A`` and ``.r``)
+    dt : float
+    constrained : int array of constrained velocity DoFs (interleaved);
+        both components of a node must be constrained together, which is
+        what ``velocity_boundary_dofs`` produces (fem.py:420-427).
+    convection : optional list of s ConvectionBlocks (row-stage Jacobians
+        J_N(u_i), stages.py:118-123); the same object repeated means one
+        shared Jacobian.
+    """
+
+    def __init__(self, blocks, tableau, dt, constrained=None, convection=None):
+        if dt < 0.0:
+            raise ValueError("timestep must be nonnegative")
+        if not isinstance(blocks, StokesBlocks):
+            raise TypeError("blocks must be a StokesBlocks (scalar-node form)")
+        self.blocks = blocks
+        self.tableau = tableau
+        self.dt = float(dt)
+        self.n_nodes = blocks.n_nodes
+        self.n_u = blocks.n_u
+        self.n_p = blocks.n_p
+        self.r = tableau.r
+        if not 1 <= self.r <= _lib.IVK_MAX_STAGES:
+            raise ValueError(f"{self.r} stages unsupported (max {_lib.IVK_MAX_STAGES})")
+        self.constrained = np.asarray(constrained if constrained is not None else [],
+                                      dtype=np.int64)
+        if convection is not None and len(convection) != self.r:
+            raise ValueError("one convection Jacobian per stage required")
+
+        c = self.constrained
+        node_mask = np.zeros(self.n_nodes, dtype=bool)
+        if len(c):
+            if c.min() < 0 or c.max() >= self.n_u:
+                raise ValueError("constrained DoF out of range")
+            nodes = np.unique(c // 2)
+            full = np.sort(np.concatenate([2 * nodes, 2 * nodes + 1]))
+            if not np.array_equal(full, np.unique(c)):
+                raise ValueError("both velocity components of a constrained node must be "
+                                 "constrained (node-level Dirichlet elimination)")
+            node_mask[nodes] = True
+        self.node_constrained = node_mask
+        self._cmask = np.repeat(node_mask, 2)
+
+        # Elimination D A D / D B (stages.py:77-85, fem.py:304-315), on the
+        # scalar pattern: zero every entry touching a constrained node.
+        rows = np.repeat(np.arange(self.n_nodes), np.diff(blocks.rowptr))
+        keep = ~(node_mask[rows] | node_mask[blocks.col])
+        self._m = np.where(keep, blocks.m, 0.0)
+        self._k = np.where(keep, blocks.k, 0.0)
+        brows = np.repeat(np.arange(self.n_nodes), np.diff(blocks.b_rowptr))
+        self._b = np.where(node_mask[brows][:, None], 0.0, blocks.b_val)
+        self._brows = brows
+
+        self.convection = None
+        self._conv_vals = None
+        if convection is not None:
+            for J in convection:
+                if not isinstance(J, ConvectionBlocks):
+                    raise TypeError("convection entries must be ConvectionBlocks")
+                if not (np.array_equal(J.rowptr, blocks.rowptr) and np.array_equal(J.col, blocks.col)):
+                    raise ValueError("convection Jacobian is not on the scalar P2 pattern")
+            shared = all(J is convection[0] for J in convection)
+            uniq = [convection[0]] if shared else list(convection)
+            self._conv_vals = [np.where(keep[:, None, None], J.val, 0.0) for J in uniq]
+            self.convection = list(convection)
+        self._dev = None
+
+    # -- layout helpers (stages.py:92-106, 169-186) -------------------------
+
+    @property
+    def stage_dim(self):
+        return self.n_u + self.n_p
+
+    @property
+    def dim(self):
+        return self.r * self.stage_dim
+
+    def split(self, x):
+        blocks = np.asarray(x).reshape(self.r, self.stage_dim)
+        return blocks[:, :self.n_u], blocks[:, self.n_u:]
+
+    def join(self, u, p):
+        return np.hstack([u, p]).ravel()
+
+    def constrained_stage_dofs(self):
+        offs = np.arange(self.r) * self.stage_dim
+        return (offs[:, None] + self.constrained[None, :]).ravel()
+
+    def project_pressure_means(self, x):
+        """Remove the per-stage constant pressure in place; returns ``x``.
+
+        Device tensors are projected by libivk; numpy arrays on the host."""
+        from ._device import is_device, ptr, stream
+        if is_device(x):
+            self.device_data()
+            _lib.check(_lib.lib().ivk_project_pressure_means(
+                self.r, self.n_u, self.n_p, ptr(x), stream()), "project_pressure_means")
+            return x
+        _, p = self.split(x)
+        p -= p.mean(axis=1, keepdims=True)
+        return x
+
+    def pressure_nullspace(self):
+        Z = np.zeros((self.dim, self.r))
+        for i in range(self.r):
+            lo = i * self.stage_dim + self.n_u
+            Z[lo:lo + self.n_p, i] = 1.0 / np.sqrt(self.n_p)
+        return Z
+
+    # -- eliminated vector-P2 views (reference layout, host) -----------------
+
+    def _scalar(self, vals):
+        b = self.blocks
+        return sp.csr_matrix((vals, b.col, b.rowptr), shape=(self.n_nodes, self.n_nodes))
+
+    @property
+    def M(self):
+        return sp.kron(self._scalar(self._m), sp.identity(2), format="csr")
+
+    @property
+    def K(self):
+        return sp.kron(self._scalar(self._k), sp.identity(2), format="csr")
+
+    @property
+    def B(self):
+        r = np.concatenate([2 * self._brows, 2 * self._brows + 1])
+        c = np.concatenate([self.blocks.b_col, self.blocks.b_col]).astype(np.int64)
+        v = np.concatenate([self._b[:, 0], self._b[:, 1]])
+        return sp.csr_matrix((v, (r, c)), shape=(self.n_u, self.n_p))
+
+    @property
+    def BT(self):
+        return self.B.T.tocsr()
+
+    def convection_matrices(self):
+        """Eliminated per-stage vector Jacobians (reference ``self.convection``)."""
+        if self.convection is None:
+            return None
+        mats = []
+        for v in self._conv_vals:
+            J = ConvectionBlocks(self.n_nodes, self.blocks.rowptr, self.blocks.col, v)
+            mats.append(J.matrix)
+        return mats * self.r if len(mats) == 1 else mats
+
+    def materialize(self, raw=False, limit=10_000):
+        """Explicit sparse stage matrix (stages.py:139-167); small systems only."""
+        if self.dim > limit:
+            raise ValueError(f"refusing to materialize {self.dim} stage dofs")
+        if raw:
+            M, K, B = self.blocks.M, self.blocks.K, self.blocks.B
+        else:
+            M, K, B = self.M, self.K, self.B
+        saddle = sp.bmat([[K, B], [B.T, None]], format="csr")
+        massd = sp.block_diag([M, sp.csr_matrix((self.n_p, self.n_p))], format="csr")
+        A = self.tableau.A
+        out = (sp.kron(sp.identity(self.r), massd) + self.dt * sp.kron(A, saddle)).tolil()
+        if self.convection is not None:
+            if raw:
+                raise ValueError("raw materialization is not defined with convection")
+            conv = self.convection_matrices()
+            sd = self.stage_dim
+            for i in range(self.r):
+                for j in range(self.r):
+                    out[i * sd:i * sd + self.n_u, j * sd:j * sd + self.n_u] += \
+                        self.dt * A[i, j] * conv[i]
+        out = out.tocsr()
+        if not raw and len(self.constrained):
+            ones = np.zeros(self.dim)
+            ones[self.constrained_stage_dofs()] = 1.0
+            out = out + sp.diags(ones)
+        return out.tocsr()
+
+    # -- device data and the K1 apply ---------------------------------------
+
+    def device_data(self):
+        """Upload the eliminated operator once; returns the descriptor."""
+        if self._dev is not None:
+            return self._dev
+        from ._device import upload
+        import torch
+        b = self.blocks
+        t = {}
+        t["p2_rowptr"] = upload(b.rowptr, np.int32)
+        t["p2_col"] = upload(b.col, np.int32)
+        t["p2_mk"] = upload(np.column_stack([self._m, self._k]), np.float64)
+        t["b_rowptr"] = upload(b.b_rowptr, np.int32)
+        t["b_col"] = upload(b.b_col, np.int32)
+        t["b_val"] = upload(self._b, np.float64)
+        # B^T rows per P1 node with (B_x, B_y) pairs -- the eliminated B (so
+        # constrained velocities drop out, stages.py:81,125).
+        order = np.lexsort((self._brows, b.b_col))
+        bt_rowptr = np.concatenate([[0], np.cumsum(np.bincount(b.b_col, minlength=self.n_p))])
+        t["bt_rowptr"] = upload(bt_rowptr, np.int32)
+        t["bt_col"] = upload(self._brows[order], np.int32)
+        t["bt_val"] = upload(self._b[order], np.float64)
+        t["cmask"] = upload(self.node_constrained.astype(np.uint8), np.uint8)
+        n_conv = 0
+        if self._conv_vals is not None:
+            t["conv"] = upload(np.stack(self._conv_vals).reshape(len(self._conv_vals), -1, 4),
+                               np.float64)
+            n_conv = len(self._conv_vals)
+        desc = _lib.OperatorDesc()
+        desc.stages = self.r
+        desc.n_nodes = self.n_nodes
+        desc.n_p = self.n_p
+        desc.n_conv = n_conv
+        desc.nnz = len(b.col)
+        desc.dt = self.dt
+        A = np.asarray(self.tableau.A, dtype=np.float64)
+        for i in range(self.r):
+            for j in range(self.r):
+                desc.butcher_a[i * self.r + j] = A[i, j]
+        desc.p2_rowptr = t["p2_rowptr"].data_ptr()
+        desc.p2_col = t["p2_col"].data_ptr()
+        desc.p2_mk = t["p2_mk"].data_ptr()
+        desc.conv = t["conv"].data_ptr() if "conv" in t else None
+        desc.b_rowptr = t["b_rowptr"].data_ptr()
+        desc.b_col = t["b_col"].data_ptr()
+        desc.b_val = t["b_val"].data_ptr()
+        desc.bt_rowptr = t["bt_rowptr"].data_ptr()
+        desc.bt_col = t["bt_col"].data_ptr()
+        desc.bt_val = t["bt_val"].data_ptr()
+        desc.node_constrained = t["cmask"].data_ptr()
+        self._dev = {"tensors": t, "desc": desc,
+                     "cmask_dofs": torch.from_numpy(self._cmask).to(t["cmask"].device)}
+        return self._dev
+
+    @property
+    def desc(self):
+        return self.device_data()["desc"]
+
+    def apply_into(self, x, b, out):
+        """Device: out = b - A x (b is not None) or out = A x."""
+        from ._device import ptr, stream
+        _lib.check(_lib.lib().ivk_stage_apply(self.desc, ptr(x), ptr(b), ptr(out), stream()),
+                   "stage_apply")
+        return out
+
+    def matvec(self, x):
+        """Eliminated operator apply (stages.py:110-126) on the GPU.
+
+        numpy in -> numpy out (host edge); a CUDA tensor stays on the device."""
+        from ._device import as_device_vector, to_host
+        import torch
+        xd, host = as_device_vector(x, self.dim)
+        y = torch.empty_like(xd)
+        self.apply_into(xd, None, y)
+        return to_host(y) if host else y
+
+    def residual(self, x, b):
+        """b - A x on the GPU (same host/device convention as ``matvec``)."""
+        from ._device import as_device_vector, to_host
+        import torch
+        xd, host = as_device_vector(x, self.dim)
+        bd, _ = as_device_vector(b, self.dim)
+        r = torch.empty_like(xd)
+        self.apply_into(xd, bd, r)
+        return to_host(r) if host else r
+
+
+def assemble_stage_operator(blocks, tableau, dt, constrained=None, convection=None):
+    """Stage operator with Dirichlet stage constraints (stages.py:189-194)."""
+    if blocks.b_rowptr[-1] == 0 and blocks.n_p:
+        raise ValueError("inconsistent block dimensions")
+    return StageSystem(blocks, tableau, dt, constrained=constrained, convection=convection)
