@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""IRK-Vanka benchmark (BASELINE.json metric) on one B200 per rank.
+
+Workload (BASELINE config 2, the headline): 256x256 right-triangle grid
+(8x8 base, 5 red refinements), Taylor-Hood P2-P1, RadauIIA(3), dt=1/256,
+nu=1; RHS uniform[-1,1] seed 1 (constrained rows zeroed, pressure means
+removed).  One STEP = one fine-level additive Vanka sweep
+x <- x + 0.5 W sum_i R_i^T A_i^-1 R_i (b - A x) (PoU weights W: the
+BASELINE "damping 0.5" smoother), i.e. kernels K1 -> K3 -> K4.
+
+value = sweeps/s over all ranks (weak scaling: every rank runs a replica);
+also reported: stage-DOF updates/s, the V-cycle time (both smoothers), the
+full FGMRES solve, the K3 roofline, the CPU-oracle baseline and e2e (host
+numpy in/out through the public ``apply_vanka``).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = dict(name="cfg2", grid="diagonal", n0=8, level=5, mu=1.0, family="radauiia",
+              stages=3, dt=1 / 256, seed=1)
+METRIC = "IRK-Vanka fine-level sweeps/s (cfg2: 256x256 P2-P1, RadauIIA(3), dt=1/256)"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_init():
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return rank, world, local
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64,
+                     device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ----------------------------------------------------------------- CPU arm
+
+def cpu_sample(sample_patches=2048, seed=CONFIG["seed"]):
+    """Oracle (numpy/scipy restatement of the reference) on a bounded sample
+    of the cfg2 sweep: the full-size residual matvec plus the patch solve of
+    ``sample_patches`` interior patches, extrapolated to all 66,049."""
+    from oracle.irk_vanka_oracle import OraclePatches, OracleStageOperator, oracle_patch_indices
+    from paper_2202_07381_b200 import Discretization, tableau_lookup
+    from paper_2202_07381_b200.fem import velocity_boundary_dofs
+    disc = Discretization(CONFIG["n0"], CONFIG["level"], mu=CONFIG["mu"], grid=CONFIG["grid"])
+    tab = tableau_lookup(CONFIG["family"], CONFIG["stages"])
+    blk = disc.blocks[-1]
+    mesh = disc.fine_mesh
+    op = OracleStageOperator(blk.M, blk.K, blk.B, tab.A, CONFIG["dt"],
+                             velocity_boundary_dofs(mesh))
+    vels, idxs = oracle_patch_indices(mesh.cells, mesh.cell_to_edges, mesh.num_vertices, op)
+    sizes = np.array([len(i) for i in idxs])
+    interior = np.flatnonzero(sizes == sizes.max())
+    rng = np.random.default_rng(0)
+    members = np.sort(rng.choice(interior, size=min(sample_patches, len(interior)),
+                                 replace=False))
+    pat = OraclePatches(op, vels, idxs, members=members)
+    b = np.random.default_rng(seed).uniform(-1, 1, op.dim)
+    b[op.constrained_stage_dofs()] = 0.0
+    op.project_pressure_means(b)
+    w = np.ones(op.dim)
+    scale = len(idxs) / len(members)
+    return op, pat, b, w, scale, len(members), len(idxs)
+
+
+def time_cpu_sweep(op, pat, b, w, scale, reps=3):
+    """Seconds per full sweep (matvec full-size + sampled solve scaled)."""
+    x = np.zeros(op.dim)
+    best_mv, best_sa = np.inf, np.inf
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = b - op.matvec(x)
+        t1 = time.perf_counter()
+        z = pat.solve_additive(r)
+        t2 = time.perf_counter()
+        _ = x + 0.5 * w * z
+        best_mv = min(best_mv, t1 - t0)
+        best_sa = min(best_sa, t2 - t1)
+    return best_mv + scale * best_sa, best_mv, best_sa
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    op, pat, b, w, scale, n_s, n_all = cpu_sample()
+    for _ in range(args.warmup):
+        time_cpu_sweep(op, pat, b, w, scale, reps=1)
+    times = []
+    for _ in range(args.steps):
+        t, _, _ = time_cpu_sweep(op, pat, b, w, scale, reps=1)
+        times.append(t)
+    t = float(np.mean(times))
+    sample = (f"full-size residual matvec + patch solves of {n_s} of {n_all} interior patches "
+              f"(scaled x{scale:.2f}) per step")
+    line = {"impl": "reference", "metric": METRIC, "value": 1.0 / t, "unit": "sweeps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg2 fine-level IRK-Vanka sweep", "grid": "256x256 diag",
+                       "scheme": "RadauIIA(3)", "dim": op.dim},
+            "stage_dof_updates_per_s": op.dim / t,
+            "cpu_baseline": {"value": 1.0 / t, "unit": "sweeps/s", "cores": 1, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": 1.0 / t, "unit": "sweeps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+
+def algorithmic_bytes(S, tables):
+    """SURVEY.md §8(d) canonical bytes per sweep and per K3 launch."""
+    nnz_s = len(S.blocks.col)
+    nnz_b = 2 * len(S.blocks.b_col)          # individual B values
+    sm = tables.total_m
+    sm2 = int(np.sum(tables.sizes.astype(np.int64) ** 2))
+    sweep = 8 * (2 * nnz_s + nnz_b) + 4 * (nnz_s + nnz_b) + 8 * 3 * S.dim + 8 * sm2 + 4 * sm
+    # K3: inverses once, gather list, gathered r (each DoF once), local[] written
+    k3 = 8 * sm2 + 4 * sm + 8 * S.dim + 8 * sm + 4 * (tables.num_patches + 1) \
+        + 8 * tables.num_patches
+    return sweep, k3, sm, sm2
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_2202_07381_b200 import (Discretization, MGHierarchyOp, MGLevel, SmootherSpec,
+                                       apply_vanka, fgmres, tableau_lookup)
+    from paper_2202_07381_b200 import _lib
+    from paper_2202_07381_b200._device import ptr, stream
+
+    t_setup0 = time.perf_counter()
+    disc = Discretization(CONFIG["n0"], CONFIG["level"], mu=CONFIG["mu"], grid=CONFIG["grid"])
+    tab = tableau_lookup(CONFIG["family"], CONFIG["stages"])
+    t_disc = time.perf_counter() - t_setup0
+    cheb = SmootherSpec(pre=2, post=2, accel="chebyshev", cheby_a=2.0, cheby_b=8.0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    mg, S = disc.build_mg(tab, CONFIG["dt"], cheb)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    pou = SmootherSpec(pre=2, post=2, accel="richardson", omega=0.5, weighting="pou")
+    mg_pou = MGHierarchyOp([MGLevel(l.system, l.patches, pou, l.prolong) for l in mg.levels],
+                           mg.coarse)
+    fine = mg.levels[-1].patches
+    dev = fine.device_data()
+    b_h = np.random.default_rng(CONFIG["seed"]).uniform(-1, 1, S.dim)
+    b_h[S.constrained_stage_dofs()] = 0.0
+    S.project_pressure_means(b_h)
+    b = torch.from_numpy(b_h).cuda()
+    x = torch.zeros_like(b)
+    xn = torch.zeros_like(b)
+    r = torch.zeros_like(b)
+    w = fine.weights("pou")
+    L = _lib.lib()
+
+    def sweep(ev=None):
+        st = stream()
+        _lib.check(L.ivk_stage_apply(S.desc, ptr(x), ptr(b), ptr(r), st), "K1")
+        if ev is not None:
+            ev[0].record()
+        _lib.check(L.ivk_patch_apply(dev["desc"], ptr(r), ptr(dev["local"]), st), "K3")
+        if ev is not None:
+            ev[1].record()
+        _lib.check(L.ivk_patch_combine(dev["desc"], ptr(dev["local"]), ptr(x), 1.0, 0.5, ptr(w),
+                                       ptr(x), None, st), "K4")
+
+    for _ in range(args.warmup):
+        sweep()
+    torch.cuda.synchronize()
+    n0 = L.ivk_launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record()
+        for k in range(args.steps):
+            sweep(evs[k])
+        stop.record()
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = L.ivk_launch_count() - n0
+    t_step = start.elapsed_time(stop) / 1e3 / args.steps
+    t_k3 = float(np.mean([a.elapsed_time(bb) for a, bb in evs])) / 1e3
+    t_step = max_over_ranks(t_step, world)
+    finite = bool(torch.isfinite(x).all())
+
+    hbm, peak_src = peaks()
+    sweep_bytes, k3_bytes, sm, sm2 = algorithmic_bytes(S, fine.tables)
+
+    # V-cycles (graph-captured) in both smoother modes
+    vc = {}
+    for name, h in (("chebyshev", mg), ("pou_richardson", mg_pou)):
+        h.use_graph = True
+        z = h.precondition(b)
+        for _ in range(3):
+            z = h.precondition(b)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        e0.record()
+        for _ in range(reps):
+            h.precondition(b)
+        e1.record()
+        torch.cuda.synchronize()
+        vc[name] = e0.elapsed_time(e1) / reps
+
+    # Full FGMRES solve (device), both smoothers
+    solves = {}
+    for name, h in (("chebyshev", mg), ("pou_richardson", mg_pou)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, st = fgmres(S.matvec, b, precond=h.precondition, rtol=1e-8, maxiter=200, restart=50)
+        torch.cuda.synchronize()
+        solves[name] = {"iterations": st.iterations, "seconds": time.perf_counter() - t0,
+                        "relative_residual": st.relative_residual, "converged": st.converged}
+
+    # e2e: public API with pinned host buffers, H2D + sweep + D2H per step
+    xh = torch.zeros(S.dim, dtype=torch.float64).pin_memory()
+    bh = torch.from_numpy(b_h.copy()).pin_memory()
+    outh = torch.empty(S.dim, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        xd = xh.to("cuda", non_blocking=True)
+        bd = bh.to("cuda", non_blocking=True)
+        y = apply_vanka(fine, S, xd, bd, omega=0.5, weights="pou")
+        outh.copy_(y, non_blocking=True)
+
+    for _ in range(max(args.warmup, 3)):
+        e2e_step()
+    torch.cuda.synchronize()
+    e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    e_start.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e_stop.record()
+    torch.cuda.synchronize()
+    t_e2e = max_over_ranks(e_start.elapsed_time(e_stop) / 1e3 / args.steps, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        op, pat, bb, ww, scale, n_s, n_all = cpu_sample()
+        t_cpu, t_mv, t_sa = time_cpu_sweep(op, pat, bb, ww, scale, reps=3)
+        cpu = {"value": 1.0 / t_cpu, "unit": "sweeps/s", "cores": 1, "kind": "port",
+               "sample": (f"oracle: full-size residual matvec ({1e3 * t_mv:.0f} ms) + patch solves "
+                          f"of {n_s}/{n_all} interior patches ({1e3 * t_sa:.0f} ms, scaled "
+                          f"x{scale:.2f}); numpy einsum/bincount, single-threaded hot path")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": world / t_step, "unit": "sweeps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded uniform[-1,1] RHS, BASELINE config 2)",
+            "config": {"workload": "cfg2 fine-level IRK-Vanka sweep (K1->K3->K4), PoU w=0.5",
+                       "grid": "256x256 diagonal-split, 6 levels", "scheme": "RadauIIA(3)",
+                       "dt": CONFIG["dt"], "dim": S.dim, "patches": fine.num_patches,
+                       "sum_m": sm, "sum_m2": sm2,
+                       "l2": "inputs larger than L2 (7.1 GB inverse stream per step)",
+                       "parallelism": f"replicas x{world}"},
+            "stage_dof_updates_per_s": world * S.dim / t_step,
+            "roofline": {"bound": "hbm", "kernel": "ivk patch_apply (K2+K3)",
+                         "achieved": k3_bytes / t_k3 / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": k3_bytes / t_k3 / 1e9 / hbm, "traffic": None,
+                         "bytes_per_launch": k3_bytes, "avg_launch_ms": 1e3 * t_k3,
+                         "peak_source": peak_src,
+                         "sweep_bytes": sweep_bytes,
+                         "sweep_achieved_gbs": sweep_bytes / t_step / 1e9,
+                         "sweep_frac": sweep_bytes / t_step / 1e9 / hbm},
+            "cpu_baseline": cpu,
+            "e2e": {"value": world / t_e2e, "unit": "sweeps/s",
+                    "h2d_bytes_per_step": 2 * 8 * S.dim, "d2h_bytes_per_step": 8 * S.dim},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "vcycle_ms": vc,
+            "fgmres": solves,
+            "setup_s": {"discretization": t_disc, "build_mg_gpu_factor": t_build},
+            "finite": finite,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    rank, world, local = dist_init()
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_ours(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

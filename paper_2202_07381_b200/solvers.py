@@ -421,6 +421,10 @@ class MGHierarchyOp:
         self.use_graph = use_graph
         self._bufs = None
         self._graph = None
+        # Parity-protocol hooks: record per-level intermediates
+        # into a dict, and/or replace the coarse output by a given vector.
+        self.trace = None
+        self.coarse_override = None
 
     @property
     def finest(self):
@@ -489,19 +493,32 @@ class MGHierarchyOp:
 
     def _cycle(self, level, x, b):
         """In place: x <- V-cycle(level, x, b) (solvers.py:334-347)."""
+        tr = self.trace
         if level == 0:
-            self.coarse.solve_into(b, x)
+            if self.coarse_override is not None:
+                x.copy_(self.coarse_override)
+            else:
+                self.coarse.solve_into(b, x)
+            if tr is not None:
+                tr["coarse_in"] = b.clone()
+                tr["coarse_out"] = x.clone()
             return
         lev = self.levels[level]
         buf = self._bufs[level]
         below = self._bufs[level - 1]
         self._smooth(level, x, b, lev.smoother.pre)
+        if tr is not None:
+            tr[f"pre_{level}"] = x.clone()
         lev.system.apply_into(x, b, buf.r)
         lev.prolong.restrict_into(buf.r, below.b)
+        if tr is not None:
+            tr[f"rc_{level}"] = below.b.clone()
         below.x.zero_()
         self._cycle(level - 1, below.x, below.b)
         lev.prolong.prolong_add(below.x, x)
         self._smooth(level, x, b, lev.smoother.post)
+        if tr is not None:
+            tr[f"post_{level}"] = x.clone()
 
     # -- public API ----------------------------------------------------------
 
