@@ -103,14 +103,24 @@ typedef struct ivk_transfer_desc {
 } ivk_transfer_desc;
 
 /* Coarsest-level direct solve with fixed LU factors (CoarseSolver,
- * solvers.py:271-292): P_r (A + Z Z^T) P_c = L U, L unit lower, both dense
- * row-major n x n.  Solve: project pressure means, x = P_c U^-1 L^-1 P_r b,
- * project again. */
+ * solvers.py:271-292): P_r (A + Z Z^T) P_c = L U, L unit lower.  The
+ * factors are stored tile-sparse: 32 x 32 tiles, column-major inside a tile
+ * (tile[j*32 + i] = F[32I + i][32K + j]), only nonzero off-diagonal tiles,
+ * grouped by block column K (l_colptr: tiles (I > K) of L in column K;
+ * u_colptr: tiles (I < K) of U in column K), plus all diagonal tiles.
+ * Solve: project pressure means, x = P_c U^-1 L^-1 P_r b, project again. */
 typedef struct ivk_coarse_desc {
   int32_t n;               /* = stages * (n_u + n_p)                      */
+  int32_t nb;              /* ceil(n / 32) block columns                  */
   int32_t stages, n_u, n_p;
-  const double* lower;     /* n x n                                       */
-  const double* upper;     /* n x n                                       */
+  const int32_t* l_colptr; /* nb + 1                                      */
+  const int32_t* l_row;    /* block row I of each off-diagonal L tile     */
+  const double* l_tiles;   /* 1024 doubles per tile                       */
+  const double* l_diag;    /* nb tiles (unit lower; padding = identity)   */
+  const int32_t* u_colptr;
+  const int32_t* u_row;
+  const double* u_tiles;
+  const double* u_diag;    /* nb tiles (upper; padding diagonal = 1)      */
   const int32_t* perm_r;   /* (P_r b)[perm_r[i]] = b[i]                   */
   const int32_t* perm_c;   /* x[i] = y[perm_c[i]]                         */
 } ivk_coarse_desc;

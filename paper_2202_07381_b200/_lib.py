@@ -67,8 +67,12 @@ class TransferDesc(C.Structure):
 
 class CoarseDesc(C.Structure):
     _fields_ = [
-        ("n", C.c_int32), ("stages", C.c_int32), ("n_u", C.c_int32), ("n_p", C.c_int32),
-        ("lower", C.c_void_p), ("upper", C.c_void_p),
+        ("n", C.c_int32), ("nb", C.c_int32), ("stages", C.c_int32), ("n_u", C.c_int32),
+        ("n_p", C.c_int32),
+        ("l_colptr", C.c_void_p), ("l_row", C.c_void_p), ("l_tiles", C.c_void_p),
+        ("l_diag", C.c_void_p),
+        ("u_colptr", C.c_void_p), ("u_row", C.c_void_p), ("u_tiles", C.c_void_p),
+        ("u_diag", C.c_void_p),
         ("perm_r", C.c_void_p), ("perm_c", C.c_void_p),
     ]
 

@@ -346,21 +346,29 @@ class CoarseSolver:
         self.system = system
         self._dev = None
 
+    def tiles(self):
+        """Tile-sparse (32 x 32, column-major tiles) copies of the factors."""
+        return tile_factor(self.lu.L, lower=True), tile_factor(self.lu.U, lower=False)
+
     def device_data(self):
         if self._dev is not None:
             return self._dev
         from ._device import upload
         s = self.system
+        (lc, lr, lt, ld, nb), (uc, ur, ut, ud, _) = self.tiles()
         t = {
-            "lower": upload(self.lu.L.toarray(), np.float64),
-            "upper": upload(self.lu.U.toarray(), np.float64),
+            "l_colptr": upload(lc, np.int32), "l_row": upload(lr, np.int32),
+            "l_tiles": upload(lt, np.float64), "l_diag": upload(ld, np.float64),
+            "u_colptr": upload(uc, np.int32), "u_row": upload(ur, np.int32),
+            "u_tiles": upload(ut, np.float64), "u_diag": upload(ud, np.float64),
             "perm_r": upload(self.lu.perm_r, np.int32),
             "perm_c": upload(self.lu.perm_c, np.int32),
         }
         d = _lib.CoarseDesc()
         d.n = s.dim
+        d.nb = nb
         d.stages, d.n_u, d.n_p = s.r, s.n_u, s.n_p
-        for k in ("lower", "upper", "perm_r", "perm_c"):
+        for k in t:
             setattr(d, k, t[k].data_ptr())
         self._dev = {"tensors": t, "desc": d}
         return self._dev
@@ -378,6 +386,40 @@ class CoarseSolver:
         x = torch.empty_like(bd)
         self.solve_into(bd, x)
         return to_host(x) if host else x
+
+
+def tile_factor(F, lower, tile=32):
+    """Split a triangular factor into dense tile x tile blocks (column-major
+    inside a tile), keeping only nonzero off-diagonal tiles, grouped by
+    block column.  Padding rows/columns get a unit diagonal."""
+    F = sp.csc_matrix(F)
+    n = F.shape[0]
+    nb = (n + tile - 1) // tile
+    npad = nb * tile
+    coo = F.tocoo()
+    keep = (coo.row >= coo.col) if lower else (coo.row <= coo.col)
+    r, c, v = coo.row[keep], coo.col[keep], coo.data[keep]
+    diag = np.zeros((nb, tile, tile))
+    bi, bj = r // tile, c // tile
+    on = bi == bj
+    diag[bi[on], r[on] % tile, c[on] % tile] = v[on]
+    # unit diagonal for L (implicit in SuperLU's L) and for padding rows
+    d = np.arange(npad) if lower else np.arange(n, npad)
+    diag[d // tile, d % tile, d % tile] = 1.0
+    off = ~on
+    key = bj[off].astype(np.int64) * nb + bi[off]
+    ukey, inv = np.unique(key, return_inverse=True)
+    tiles = np.zeros((len(ukey), tile, tile))
+    tiles[inv, r[off] % tile, c[off] % tile] = v[off]
+    col_of = ukey // nb
+    row_of = ukey % nb
+    colptr = np.concatenate([[0], np.cumsum(np.bincount(col_of, minlength=nb))])
+    # column-major storage inside each tile: element (i, j) at j*tile + i
+    tiles_cm = np.ascontiguousarray(np.transpose(tiles, (0, 2, 1))).reshape(-1)
+    diag_cm = np.ascontiguousarray(np.transpose(diag, (0, 2, 1))).reshape(-1)
+    if len(tiles_cm) == 0:
+        tiles_cm = np.zeros(tile * tile)
+    return colptr, row_of, tiles_cm, diag_cm, nb
 
 
 def coarse_direct_solve(system):
