@@ -121,6 +121,41 @@ class StokesBlocks:
     def n_u(self):
         return 2 * self.n_nodes
 
+    @classmethod
+    def from_vector(cls, M, K, B):
+        """Scalar-node blocks from the reference's interleaved vector-P2 CSR
+        ``BlockSystem`` (fem.py:99-113).  Requires M = M_P2 (x) I_2 and
+        K = K_P2 (x) I_2 (true for the reference's assembly, fem.py:149-154);
+        the scalar pattern is the union of M's and K's stored structure."""
+        M, K, B = sp.csr_matrix(M), sp.csr_matrix(K), sp.csr_matrix(B)
+        n_u, n_p = B.shape
+        if n_u % 2 or M.shape != (n_u, n_u) or K.shape != (n_u, n_u):
+            raise ValueError("inconsistent block dimensions")
+        n = n_u // 2
+        # The reference sums duplicate entries of the two components in
+        # independent (scipy sort) orders, so the components may differ by an
+        # ulp; the x-component values are taken.
+        for A in (M, K):
+            scale = max(abs(A).max(), 1e-300)
+            if (abs(A[1::2, 1::2] - A[0::2, 0::2]).max() > 1e-14 * scale
+                    or abs(A[0::2, 1::2]).max() > 0 or abs(A[1::2, 0::2]).max() > 0):
+                raise ValueError("velocity block is not (scalar P2) x I_2")
+        S = _structure(M[0::2, 0::2]) + _structure(K[0::2, 0::2])
+        S = sp.csr_matrix(S)
+        S.sort_indices()
+        rows = np.repeat(np.arange(n), np.diff(S.indptr))
+        m = np.asarray(M[0::2, 0::2][rows, S.indices]).ravel()
+        k = np.asarray(K[0::2, 0::2][rows, S.indices]).ravel()
+        T = sp.csr_matrix(_structure(B[0::2]) + _structure(B[1::2]))
+        T.sort_indices()
+        brows = np.repeat(np.arange(n), np.diff(T.indptr))
+        bx = np.asarray(B[0::2][brows, T.indices]).ravel()
+        by = np.asarray(B[1::2][brows, T.indices]).ravel()
+        return cls(n_nodes=n, n_p=n_p, rowptr=S.indptr.astype(np.int64),
+                   col=S.indices.astype(np.int32), m=m, k=k,
+                   b_rowptr=T.indptr.astype(np.int64), b_col=T.indices.astype(np.int32),
+                   b_val=np.column_stack([bx, by]))
+
     # Vector-P2 views in the reference's (interleaved) layout -- used by the
     # oracle, the coarse materialisation and API parity, never by kernels.
     def scalar_matrix(self, vals):
@@ -146,6 +181,13 @@ class StokesBlocks:
         return sp.csr_matrix((v, (r, c)), shape=(self.n_u, self.n_p))
 
 
+def _structure(A):
+    """0/1 matrix with A's stored (structural, incl. explicit zero) entries."""
+    A = sp.csr_matrix(A, copy=True)
+    A.data[:] = 1.0
+    return A
+
+
 @dataclass
 class ConvectionBlocks:
     """Convection Jacobian on the scalar P2 pattern: one 2x2 block per entry.
@@ -157,6 +199,22 @@ class ConvectionBlocks:
     rowptr: np.ndarray
     col: np.ndarray
     val: np.ndarray  # (nnz, 2, 2)
+
+    @classmethod
+    def from_vector(cls, J, blocks):
+        """2x2 blocks of a vector-P2 Jacobian (reference ``assemble_convection``
+        output) on ``blocks``' scalar pattern; entries off the pattern must be 0."""
+        J = sp.csr_matrix(J)
+        rows = np.repeat(np.arange(blocks.n_nodes), np.diff(blocks.rowptr))
+        col = blocks.col.astype(np.int64)
+        val = np.empty((len(col), 2, 2))
+        for d in range(2):
+            for f in range(2):
+                val[:, d, f] = np.asarray(J[2 * rows + d, 2 * col + f]).ravel()
+        out = cls(blocks.n_nodes, blocks.rowptr, blocks.col, val)
+        if abs(out.matrix - J).max() > 0:
+            raise ValueError("Jacobian has entries outside the scalar P2 pattern")
+        return out
 
     @property
     def matrix(self):
