@@ -86,7 +86,30 @@ typedef struct ivk_patch_desc {
   const int32_t* vertex;   /* num_patches: centre vertex                  */
   const int32_t* node_off; /* num_patches + 1                             */
   const int32_t* node;     /* free scalar P2 nodes of each patch, sorted  */
+  const struct ivk_kron_desc* kron; /* HOST pointer; NULL = full inverses */
 } ivk_patch_desc;
+
+/* Kronecker eigen-split of the patch matrices.  With all stages sharing one
+ * convection Jacobian the stage-coupled patch matrix is
+ *   P = I_s (x) M^ + dt A (x) S^,   M^ = [[M_l,0],[0,0]],  S^ = [[K_l+J_l, b],[b^T, 0]]
+ * (solvers.py:196-211), so with A = V diag(lam) V^-1:
+ *   P^-1 = (V (x) I) blockdiag_k (M^ + dt lam_k S^)^-1 (V^-1 (x) I).
+ * One block is stored per real eigenvalue and one per complex-conjugate pair
+ * (the conjugate block is its complex conjugate).  Per patch, block k is
+ * G_k^T (b = m / s rows): real blocks b x ldr doubles (ldr = (b+3)&~3),
+ * complex blocks b x 2*ldc doubles, (re, im) interleaved (ldc = (b+1)&~1).
+ * Back-transform: z_i = sum_k scale_k Re(V[i][k] z~_k), scale 1 (real) or 2
+ * (pair).  Inverse bytes per patch drop from (s b)^2 to s b^2 doubles. */
+typedef struct ivk_kron_desc {
+  int32_t nblk;                       /* stored eigen-blocks              */
+  int32_t is_complex[IVK_MAX_STAGES];
+  double lam_re[IVK_MAX_STAGES], lam_im[IVK_MAX_STAGES];
+  double v_re[IVK_MAX_STAGES * IVK_MAX_STAGES];    /* V[i][k], row-major    */
+  double v_im[IVK_MAX_STAGES * IVK_MAX_STAGES];
+  double vinv_re[IVK_MAX_STAGES * IVK_MAX_STAGES]; /* V^-1[k][i]           */
+  double vinv_im[IVK_MAX_STAGES * IVK_MAX_STAGES];
+  double scale[IVK_MAX_STAGES];
+} ivk_kron_desc;
 
 /* Nested P2/P1 transfer I_s (x) blockdiag(P_P2 (x) I_2, P_P1)
  * (bench.py:187-194, fem.py:255-301), fine <- coarse, plus its transpose. */

@@ -7,7 +7,7 @@ every operator raises -- there is no CPU fallback.
 import ctypes as C
 import os
 
-__all__ = ["lib", "check", "OperatorDesc", "PatchDesc", "TransferDesc", "CoarseDesc",
+__all__ = ["lib", "check", "OperatorDesc", "PatchDesc", "KronDesc", "TransferDesc", "CoarseDesc",
            "IVK_MAX_STAGES", "IvkError", "SingularPatch"]
 
 IVK_MAX_STAGES = 3
@@ -43,6 +43,19 @@ class OperatorDesc(C.Structure):
     ]
 
 
+class KronDesc(C.Structure):
+    _fields_ = [
+        ("nblk", C.c_int32),
+        ("is_complex", C.c_int32 * IVK_MAX_STAGES),
+        ("lam_re", C.c_double * IVK_MAX_STAGES), ("lam_im", C.c_double * IVK_MAX_STAGES),
+        ("v_re", C.c_double * (IVK_MAX_STAGES * IVK_MAX_STAGES)),
+        ("v_im", C.c_double * (IVK_MAX_STAGES * IVK_MAX_STAGES)),
+        ("vinv_re", C.c_double * (IVK_MAX_STAGES * IVK_MAX_STAGES)),
+        ("vinv_im", C.c_double * (IVK_MAX_STAGES * IVK_MAX_STAGES)),
+        ("scale", C.c_double * IVK_MAX_STAGES),
+    ]
+
+
 class PatchDesc(C.Structure):
     _fields_ = [
         ("num_patches", C.c_int32), ("dim", C.c_int32), ("max_m", C.c_int32),
@@ -50,6 +63,7 @@ class PatchDesc(C.Structure):
         ("idx_off", C.c_void_p), ("idx", C.c_void_p), ("inv_off", C.c_void_p),
         ("inv", C.c_void_p), ("dof_ptr", C.c_void_p), ("dof_pos", C.c_void_p),
         ("vertex", C.c_void_p), ("node_off", C.c_void_p), ("node", C.c_void_p),
+        ("kron", C.POINTER(KronDesc)),
     ]
 
 

@@ -163,6 +163,25 @@ struct FactorParams {
   const double2* __restrict__ b_val;
 };
 
+static FactorParams make_factor_params(const ivk_operator_desc* op) {
+  FactorParams f;
+  f.n_nodes = op->n_nodes;
+  f.n_p = op->n_p;
+  f.n_conv = op->n_conv;
+  f.nnz = op->nnz;
+  f.S = op->stages;
+  f.dt = op->dt;
+  for (int i = 0; i < IVK_MAX_STAGES * IVK_MAX_STAGES; ++i) f.a[i] = op->butcher_a[i];
+  f.p2_rowptr = op->p2_rowptr;
+  f.p2_col = op->p2_col;
+  f.p2_mk = reinterpret_cast<const double2*>(op->p2_mk);
+  f.conv = reinterpret_cast<const double4*>(op->conv);
+  f.b_rowptr = op->b_rowptr;
+  f.b_col = op->b_col;
+  f.b_val = reinterpret_cast<const double2*>(op->b_val);
+  return f;
+}
+
 // Position of `col` in the sorted CSR row [lo, hi), or -1.
 __device__ __forceinline__ int find_col(const int32_t* __restrict__ cols, int lo, int hi, int col) {
   while (lo < hi) {
@@ -310,6 +329,365 @@ __global__ void __launch_bounds__(kFactorThreads) patch_factor_kernel(FactorPara
   }
 }
 
+
+// ---------------------------------------------------------- Kronecker split
+//
+// K7e / K3e: the eigen-split formulation (include/ivk.h, ivk_kron_desc).
+
+struct KronParams {
+  int nblk, S;
+  int is_complex[IVK_MAX_STAGES];
+  double lam_re[IVK_MAX_STAGES], lam_im[IVK_MAX_STAGES];
+  double v_re[IVK_MAX_STAGES * IVK_MAX_STAGES], v_im[IVK_MAX_STAGES * IVK_MAX_STAGES];
+  double vinv_re[IVK_MAX_STAGES * IVK_MAX_STAGES], vinv_im[IVK_MAX_STAGES * IVK_MAX_STAGES];
+  double scale[IVK_MAX_STAGES];
+};
+
+static KronParams make_kron(const ivk_kron_desc* k, int S) {
+  KronParams p;
+  p.nblk = k->nblk;
+  p.S = S;
+  for (int i = 0; i < IVK_MAX_STAGES; ++i) {
+    p.is_complex[i] = k->is_complex[i];
+    p.lam_re[i] = k->lam_re[i];
+    p.lam_im[i] = k->lam_im[i];
+    p.scale[i] = k->scale[i];
+  }
+  for (int i = 0; i < IVK_MAX_STAGES * IVK_MAX_STAGES; ++i) {
+    p.v_re[i] = k->v_re[i];
+    p.v_im[i] = k->v_im[i];
+    p.vinv_re[i] = k->vinv_re[i];
+    p.vinv_im[i] = k->vinv_im[i];
+  }
+  return p;
+}
+
+__host__ __device__ __forceinline__ int kron_ldr(int b) { return (b + 3) & ~3; }
+__host__ __device__ __forceinline__ int kron_ldc(int b) { return (b + 1) & ~1; }
+
+// In-place Gauss-Jordan inverse (row pivoting, first max of |re|+|im|) of a
+// d x d matrix held as separate re/im arrays in shared memory.
+template <bool CPLX>
+__device__ bool gauss_jordan(double* Are, double* Aim, int d, int* piv, double* colre,
+                             double* colim, int* s_prow, int* s_bad) {
+  const int tid = threadIdx.x;
+  for (int k = 0; k < d; ++k) {
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + tid; i < d; i += 32) {
+        double a = fabs(Are[i * d + k]);
+        if (CPLX) a += fabs(Aim[i * d + k]);
+        if (a > best) { best = a; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_down_sync(0xffffffffu, best, o);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tid == 0) {
+        *s_prow = bi;
+        piv[k] = bi;
+        if (!(best > 0.0)) *s_bad = 1;
+      }
+    }
+    __syncthreads();
+    if (*s_bad) return false;
+    const int pr = *s_prow;
+    if (pr != k) {
+      for (int j = tid; j < d; j += blockDim.x) {
+        double t = Are[k * d + j]; Are[k * d + j] = Are[pr * d + j]; Are[pr * d + j] = t;
+        if (CPLX) { t = Aim[k * d + j]; Aim[k * d + j] = Aim[pr * d + j]; Aim[pr * d + j] = t; }
+      }
+      __syncthreads();
+    }
+    double pr_re = Are[k * d + k], pr_im = CPLX ? Aim[k * d + k] : 0.0;
+    double inv_re, inv_im = 0.0;
+    if (CPLX) {
+      const double den = pr_re * pr_re + pr_im * pr_im;
+      inv_re = pr_re / den;
+      inv_im = -pr_im / den;
+    } else {
+      inv_re = 1.0 / pr_re;
+    }
+    for (int i = tid; i < d; i += blockDim.x) {
+      colre[i] = (i == k) ? 0.0 : Are[i * d + k];
+      if (CPLX) colim[i] = (i == k) ? 0.0 : Aim[i * d + k];
+    }
+    __syncthreads();
+    for (int j = tid; j < d; j += blockDim.x) {
+      if (j == k) {
+        Are[k * d + k] = inv_re;
+        if (CPLX) Aim[k * d + k] = inv_im;
+      } else if (CPLX) {
+        const double a = Are[k * d + j], b = Aim[k * d + j];
+        Are[k * d + j] = a * inv_re - b * inv_im;
+        Aim[k * d + j] = a * inv_im + b * inv_re;
+      } else {
+        Are[k * d + j] *= inv_re;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < d * d; e += blockDim.x) {
+      const int i = e / d, j = e - i * d;
+      if (i == k) continue;
+      const double fr = colre[i];
+      const double br = (j == k) ? 0.0 : Are[e];
+      const double pr2 = Are[k * d + j];
+      if (CPLX) {
+        const double fi = colim[i];
+        const double bi = (j == k) ? 0.0 : Aim[e];
+        const double pi2 = Aim[k * d + j];
+        Are[e] = br - (fr * pr2 - fi * pi2);
+        Aim[e] = bi - (fr * pi2 + fi * pr2);
+      } else {
+        Are[e] = br - fr * pr2;
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = d - 1; k >= 0; --k) {
+    const int pk = piv[k];
+    if (pk != k) {
+      for (int i = tid; i < d; i += blockDim.x) {
+        double t = Are[i * d + k]; Are[i * d + k] = Are[i * d + pk]; Are[i * d + pk] = t;
+        if (CPLX) { t = Aim[i * d + k]; Aim[i * d + k] = Aim[i * d + pk]; Aim[i * d + pk] = t; }
+      }
+      __syncthreads();
+    }
+  }
+  return true;
+}
+
+constexpr int kKronFactorThreads = 256;
+
+// One CTA per patch; for every stored eigen-block assemble M^ + dt lam S^
+// (b x b) and invert it.  Dynamic smem: 2 * bmax^2 doubles.
+__global__ void __launch_bounds__(kKronFactorThreads) patch_factor_kron_kernel(
+    FactorParams op, PatchParams pd, KronParams kp, int32_t* singular) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int piv[256];
+  __shared__ double colre[256], colim[256];
+  __shared__ int s_prow, s_bad;
+  const int p = blockIdx.x;
+  const int n0 = pd.node_off[p], nk = pd.node_off[p + 1] - n0;
+  const int* nodes = pd.node + n0;
+  const int v = pd.vertex[p];
+  const int mv = 2 * nk, b = mv + 1;
+  const int tid = threadIdx.x;
+  double* Are = sm;
+  double* Aim = sm + b * b;
+  double* out = pd.inv + pd.inv_off[p];
+  if (tid == 0) s_bad = 0;
+  for (int k = 0; k < kp.nblk; ++k) {
+    const bool cplx = kp.is_complex[k] != 0;
+    const double fre = op.dt * kp.lam_re[k], fim = op.dt * kp.lam_im[k];
+    for (int e = tid; e < b * b; e += blockDim.x) { Are[e] = 0.0; Aim[e] = 0.0; }
+    __syncthreads();
+    for (int pr = tid; pr < nk * nk; pr += blockDim.x) {
+      const int al = pr / nk, be = pr % nk;
+      const int row = nodes[al];
+      const int pos = find_col(op.p2_col, op.p2_rowptr[row], op.p2_rowptr[row + 1], nodes[be]);
+      if (pos < 0) continue;
+      const double2 mk = op.p2_mk[pos];
+      double4 J = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (op.n_conv >= 1) J = op.conv[pos];
+      // S^ entries of the 2x2 node block, then M^ + dt lam S^
+      const double s00 = mk.y + J.x, s01 = J.y, s10 = J.z, s11 = mk.y + J.w;
+      const int r0 = 2 * al, c0 = 2 * be;
+      Are[r0 * b + c0] = mk.x + fre * s00;
+      Are[r0 * b + c0 + 1] = fre * s01;
+      Are[(r0 + 1) * b + c0] = fre * s10;
+      Are[(r0 + 1) * b + c0 + 1] = mk.x + fre * s11;
+      Aim[r0 * b + c0] = fim * s00;
+      Aim[r0 * b + c0 + 1] = fim * s01;
+      Aim[(r0 + 1) * b + c0] = fim * s10;
+      Aim[(r0 + 1) * b + c0 + 1] = fim * s11;
+    }
+    for (int al = tid; al < nk; al += blockDim.x) {
+      const int row = nodes[al];
+      const int pos = find_col(op.b_col, op.b_rowptr[row], op.b_rowptr[row + 1], v);
+      const double2 bv = pos >= 0 ? op.b_val[pos] : make_double2(0.0, 0.0);
+      const int r0 = 2 * al;
+      Are[r0 * b + mv] = fre * bv.x;
+      Are[(r0 + 1) * b + mv] = fre * bv.y;
+      Are[mv * b + r0] = fre * bv.x;
+      Are[mv * b + r0 + 1] = fre * bv.y;
+      Aim[r0 * b + mv] = fim * bv.x;
+      Aim[(r0 + 1) * b + mv] = fim * bv.y;
+      Aim[mv * b + r0] = fim * bv.x;
+      Aim[mv * b + r0 + 1] = fim * bv.y;
+    }
+    __syncthreads();
+    const bool ok = cplx ? gauss_jordan<true>(Are, Aim, b, piv, colre, colim, &s_prow, &s_bad)
+                         : gauss_jordan<false>(Are, Aim, b, piv, colre, colim, &s_prow, &s_bad);
+    if (!ok) {
+      if (tid == 0) atomicMin(singular, v);
+      return;
+    }
+    // store G^T
+    if (cplx) {
+      const int ldc = kron_ldc(b);
+      for (int e = tid; e < b * ldc; e += blockDim.x) {
+        const int j = e / ldc, i = e - j * ldc;
+        const bool in = i < b;
+        out[2 * e] = in ? Are[i * b + j] : 0.0;
+        out[2 * e + 1] = in ? Aim[i * b + j] : 0.0;
+      }
+      out += 2 * b * ldc;
+    } else {
+      const int ldr = kron_ldr(b);
+      for (int e = tid; e < b * ldr; e += blockDim.x) {
+        const int j = e / ldr, i = e - j * ldr;
+        out[e] = (i < b) ? Are[i * b + j] : 0.0;
+      }
+      out += b * ldr;
+    }
+    __syncthreads();
+  }
+}
+
+// Warp per patch.  Gather r_p, transform to the eigenbasis, one streamed
+// GEMV per stored block (lanes split into G groups of CPC lanes; each lane
+// owns a 32-byte row chunk, groups take interleaved columns), back-transform.
+template <int MAXB>
+__global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_kernel(
+    PatchParams pd, KronParams kp, const double* __restrict__ r, double* __restrict__ local) {
+  constexpr int MAXM = IVK_MAX_STAGES * MAXB;
+  __shared__ __align__(16) double rs_all[kApplyWarps][MAXM];
+  __shared__ __align__(16) double rt_all[kApplyWarps][IVK_MAX_STAGES][2 * MAXB];
+  __shared__ __align__(16) double red_all[kApplyWarps][32 * 4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* rs = rs_all[warp];
+  double* red = red_all[warp];
+  const int S = kp.S;
+  const int stride = gridDim.x * kApplyWarps;
+  for (int p = blockIdx.x * kApplyWarps + warp; p < pd.num_patches; p += stride) {
+    const int off = pd.idx_off[p];
+    const int m = pd.idx_off[p + 1] - off;
+    const int b = m / S;
+    for (int j = lane; j < m; j += 32) rs[j] = __ldg(r + pd.idx[off + j]);
+    __syncwarp();
+    // r~_k[a] = sum_i Vinv[k][i] r[i][a]
+    for (int e = lane; e < kp.nblk * b; e += 32) {
+      const int k = e / b, a = e - k * b;
+      double re = 0.0, im = 0.0;
+      for (int i = 0; i < S; ++i) {
+        const double x = rs[i * b + a];
+        re = fma(kp.vinv_re[k * S + i], x, re);
+        im = fma(kp.vinv_im[k * S + i], x, im);
+      }
+      rt_all[warp][k][2 * a] = re;
+      rt_all[warp][k][2 * a + 1] = im;
+    }
+    __syncwarp();
+    const double* G = pd.inv + pd.inv_off[p];
+    for (int k = 0; k < kp.nblk; ++k) {
+      double* rt = rt_all[warp][k];
+      const bool cplx = kp.is_complex[k] != 0;
+      const int ldd = cplx ? 2 * kron_ldc(b) : kron_ldr(b);  // doubles per column
+      const int cpc = ldd >> 2;                               // 32-byte chunks per column
+      const int groups = 32 / cpc;
+      const int g = lane / cpc, c = lane - g * cpc;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (g < groups) {
+        const double* col = G + 4 * c;
+        int j = g;
+        if (cplx) {
+          for (; j + 3 * groups < b; j += 4 * groups) {
+            double v[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              ld_stream4(col + (long)(j + u * groups) * ldd, v[u][0], v[u][1], v[u][2], v[u][3]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double xr = rt[2 * (j + u * groups)], xi = rt[2 * (j + u * groups) + 1];
+              a0 = fma(v[u][0], xr, fma(-v[u][1], xi, a0));
+              a1 = fma(v[u][0], xi, fma(v[u][1], xr, a1));
+              a2 = fma(v[u][2], xr, fma(-v[u][3], xi, a2));
+              a3 = fma(v[u][2], xi, fma(v[u][3], xr, a3));
+            }
+          }
+          for (; j < b; j += groups) {
+            double v0, v1, v2, v3;
+            ld_stream4(col + (long)j * ldd, v0, v1, v2, v3);
+            const double xr = rt[2 * j], xi = rt[2 * j + 1];
+            a0 = fma(v0, xr, fma(-v1, xi, a0));
+            a1 = fma(v0, xi, fma(v1, xr, a1));
+            a2 = fma(v2, xr, fma(-v3, xi, a2));
+            a3 = fma(v2, xi, fma(v3, xr, a3));
+          }
+        } else {
+          for (; j + 3 * groups < b; j += 4 * groups) {
+            double v[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              ld_stream4(col + (long)(j + u * groups) * ldd, v[u][0], v[u][1], v[u][2], v[u][3]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double x = rt[2 * (j + u * groups)];
+              a0 = fma(v[u][0], x, a0);
+              a1 = fma(v[u][1], x, a1);
+              a2 = fma(v[u][2], x, a2);
+              a3 = fma(v[u][3], x, a3);
+            }
+          }
+          for (; j < b; j += groups) {
+            double v0, v1, v2, v3;
+            ld_stream4(col + (long)j * ldd, v0, v1, v2, v3);
+            const double x = rt[2 * j];
+            a0 = fma(v0, x, a0);
+            a1 = fma(v1, x, a1);
+            a2 = fma(v2, x, a2);
+            a3 = fma(v3, x, a3);
+          }
+        }
+      }
+      red[4 * lane + 0] = a0;
+      red[4 * lane + 1] = a1;
+      red[4 * lane + 2] = a2;
+      red[4 * lane + 3] = a3;
+      __syncwarp();
+      // z~_k[a] = sum over groups; overwrite rt[k] (no longer needed)
+      if (cplx) {
+        for (int a = lane; a < b; a += 32) {
+          const int ch = a >> 1, q = (a & 1) * 2;
+          double re = 0.0, im = 0.0;
+          for (int gg = 0; gg < groups; ++gg) {
+            re += red[4 * (gg * cpc + ch) + q];
+            im += red[4 * (gg * cpc + ch) + q + 1];
+          }
+          rt[2 * a] = re;
+          rt[2 * a + 1] = im;
+        }
+        G += 2L * b * kron_ldc(b);
+      } else {
+        for (int a = lane; a < b; a += 32) {
+          const int ch = a >> 2, q = a & 3;
+          double re = 0.0;
+          for (int gg = 0; gg < groups; ++gg) re += red[4 * (gg * cpc + ch) + q];
+          rt[2 * a] = re;
+          rt[2 * a + 1] = 0.0;
+        }
+        G += (long)b * kron_ldr(b);
+      }
+      __syncwarp();
+    }
+    // z[i][a] = sum_k scale_k Re(V[i][k] z~_k[a])
+    for (int e = lane; e < m; e += 32) {
+      const int i = e / b, a = e - i * b;
+      double acc = 0.0;
+      for (int k = 0; k < kp.nblk; ++k) {
+        const double zr = rt_all[warp][k][2 * a], zi = rt_all[warp][k][2 * a + 1];
+        acc += kp.scale[k] * (kp.v_re[i * S + k] * zr - kp.v_im[i * S + k] * zi);
+      }
+      local[off + e] = acc;
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace ivk
 
 using namespace ivk;
@@ -326,6 +704,21 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
   const int cap = kSMs * 8;  // persistent-ish: 8 CTAs (64 warps) per SM
   if (grid > cap) grid = cap;
   cudaStream_t st = as_stream(stream);
+  if (pd->kron) {
+    const ivk_kron_desc* k = pd->kron;
+    IVK_REQUIRE(k->nblk >= 1 && k->nblk <= IVK_MAX_STAGES, "bad kron block count");
+    int S = 0;
+    for (int i = 0; i < k->nblk; ++i) S += k->is_complex[i] ? 2 : 1;
+    KronParams kp = make_kron(k, S);
+    const int bmax = pd->max_m / S;
+    if (bmax <= 64)
+      patch_apply_kron_kernel<64><<<grid, kApplyWarps * 32, 0, st>>>(p, kp, r, local);
+    else {
+      set_error("ivk_patch_apply: kron block size %d > 64 unsupported", bmax);
+      return IVK_EUNSUPPORTED;
+    }
+    return check_launch("ivk_patch_apply(kron)");
+  }
   if (pd->max_m <= 128)
     patch_apply_kernel<128><<<grid, kApplyWarps * 32, 0, st>>>(p, r, local);
   else if (pd->max_m <= 256)
@@ -359,6 +752,32 @@ int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int3
   if (rc) return rc;
   IVK_REQUIRE(pd->vertex && pd->node_off && pd->node && singular_dev,
               "patch factorisation needs vertex/node tables and a singular flag");
+  if (pd->kron) {
+    const ivk_kron_desc* k = pd->kron;
+    int S = 0;
+    for (int i = 0; i < k->nblk; ++i) S += k->is_complex[i] ? 2 : 1;
+    IVK_REQUIRE(S == op->stages, "kron blocks do not cover %d stages", op->stages);
+    IVK_REQUIRE(op->n_conv <= 1, "kron split needs one convection Jacobian shared by all stages");
+    const int bmax = pd->max_m / S;
+    IVK_REQUIRE(bmax <= 64, "kron block size %d > 64 unsupported", bmax);
+    const size_t smem = 2 * (size_t)bmax * bmax * sizeof(double);
+    static size_t configured = 0;
+    if (smem > configured) {
+      cudaError_t e = cudaFuncSetAttribute(patch_factor_kron_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) {
+        set_error("ivk_patch_factor: %s", cudaGetErrorString(e));
+        return IVK_ECUDA;
+      }
+      configured = smem;
+    }
+    FactorParams f = make_factor_params(op);
+    PatchParams p = make_patch_params(pd);
+    KronParams kp = make_kron(k, S);
+    patch_factor_kron_kernel<<<pd->num_patches, kKronFactorThreads, smem, as_stream(stream)>>>(
+        f, p, kp, singular_dev);
+    return check_launch("ivk_patch_factor(kron)");
+  }
   const int dmax = pd->max_m;
   if (dmax > 512) {
     set_error("ivk_patch_factor: patch size %d > 512 unsupported", dmax);
@@ -375,21 +794,7 @@ int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int3
     set_error("ivk_patch_factor: %s", cudaGetErrorString(e));
     return IVK_ECUDA;
   }
-  FactorParams f;
-  f.n_nodes = op->n_nodes;
-  f.n_p = op->n_p;
-  f.n_conv = op->n_conv;
-  f.nnz = op->nnz;
-  f.S = op->stages;
-  f.dt = op->dt;
-  for (int i = 0; i < IVK_MAX_STAGES * IVK_MAX_STAGES; ++i) f.a[i] = op->butcher_a[i];
-  f.p2_rowptr = op->p2_rowptr;
-  f.p2_col = op->p2_col;
-  f.p2_mk = reinterpret_cast<const double2*>(op->p2_mk);
-  f.conv = reinterpret_cast<const double4*>(op->conv);
-  f.b_rowptr = op->b_rowptr;
-  f.b_col = op->b_col;
-  f.b_val = reinterpret_cast<const double2*>(op->b_val);
+  FactorParams f = make_factor_params(op);
   PatchParams p = make_patch_params(pd);
   patch_factor_kernel<<<pd->num_patches, kFactorThreads, smem, as_stream(stream)>>>(f, p,
                                                                                     singular_dev);

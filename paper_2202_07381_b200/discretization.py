@@ -57,7 +57,8 @@ class Discretization:
                                                      self.cnodes[level - 1])
         return self._stage_prolong[key]
 
-    def build_mg(self, tableau, dt, smoother, mg_levels=None, convection=None, use_graph=False):
+    def build_mg(self, tableau, dt, smoother, mg_levels=None, convection=None, use_graph=False,
+                 patch_mode="auto"):
         """Stage systems on every level, GPU-factorised Vanka patches and the
         V-cycle (bench.py:206-228).  Returns (MGHierarchyOp, finest system)."""
         total = self.num_levels
@@ -73,7 +74,8 @@ class Discretization:
             # The coarsest level's patches are never used (direct solve); the
             # reference builds them anyway (bench.py:224) -- we skip the
             # factorisation there.
-            patches = VankaPatchSet(system, self.hier.levels[k], factor=(k > start))
+            patches = VankaPatchSet(system, self.hier.levels[k], factor=(k > start),
+                                    mode=patch_mode)
             P = self.stage_prolong(k, tableau.r) if k > start else None
             levels.append(MGLevel(system, patches, smoother, P))
         coarse = coarse_direct_solve(levels[0].system)

@@ -24,6 +24,8 @@ import numpy as np
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
+import ctypes as C
+
 from . import _lib
 from .patches import build_patch_tables
 
@@ -88,6 +90,71 @@ class KrylovStats:
 
 # ----------------------------------------------------------------- patches
 
+class KronSplit:
+    """Eigen-split A = V diag(lam) V^-1 of the Butcher matrix (include/ivk.h,
+    ``ivk_kron_desc``): one stored block per real eigenvalue and per
+    complex-conjugate pair."""
+
+    def __init__(self, A, max_cond=1e6):
+        A = np.asarray(A, dtype=np.float64)
+        s = len(A)
+        lam, V = np.linalg.eig(A)
+        if not np.all(np.isfinite(V)) or np.linalg.cond(V) > max_cond:
+            raise ValueError("Butcher matrix is not (well) diagonalisable")
+        Vinv = np.linalg.inv(V)
+        tol = 1e-12 * max(1.0, np.max(np.abs(lam)))
+        real = [k for k in range(s) if abs(lam[k].imag) <= tol]
+        pos = [k for k in range(s) if lam[k].imag > tol]
+        if len(real) + 2 * len(pos) != s:
+            raise ValueError("unpaired complex eigenvalues")
+        keep = real + pos
+        self.s = s
+        self.lam = lam[keep]
+        self.is_complex = np.array([0] * len(real) + [1] * len(pos), dtype=np.int32)
+        self.V = V[:, keep]
+        self.Vinv = Vinv[keep, :]
+        for k in range(len(real)):
+            self.lam[k] = self.lam[k].real
+            self.V[:, k] = self.V[:, k].real
+            self.Vinv[k, :] = self.Vinv[k, :].real
+        self.scale = np.where(self.is_complex == 1, 2.0, 1.0)
+
+    @property
+    def nblk(self):
+        return len(self.lam)
+
+    def desc(self):
+        d = _lib.KronDesc()
+        d.nblk = self.nblk
+        for k in range(self.nblk):
+            d.is_complex[k] = int(self.is_complex[k])
+            d.lam_re[k] = self.lam[k].real
+            d.lam_im[k] = self.lam[k].imag
+            d.scale[k] = self.scale[k]
+            for i in range(self.s):
+                d.v_re[i * self.s + k] = self.V[i, k].real
+                d.v_im[i * self.s + k] = self.V[i, k].imag
+                d.vinv_re[k * self.s + i] = self.Vinv[k, i].real
+                d.vinv_im[k * self.s + i] = self.Vinv[k, i].imag
+        return d
+
+    def block_doubles(self, b):
+        """Stored doubles per patch of block size b (matches the kernels)."""
+        ldr = (b + 3) & ~3
+        ldc = (b + 1) & ~1
+        return sum(2 * b * ldc if c else b * ldr for c in self.is_complex)
+
+    def full_inverse(self, G, b):
+        """Reassemble the (s b) x (s b) inverse from stored blocks G[k] (b x b)."""
+        s = self.s
+        out = np.zeros((s * b, s * b))
+        for k in range(self.nblk):
+            T = self.scale[k] * np.real(np.einsum("i,ac,j->iajc", self.V[:, k], G[k],
+                                                  self.Vinv[k, :]))
+            out += T.reshape(s * b, s * b)
+        return out
+
+
 class VankaPatchSet:
     """Vertex-star patches with device-resident dense inverses (solvers.py:116-222).
 
@@ -95,18 +162,50 @@ class VankaPatchSet:
     components, all stages) on the closure of the vertex star plus the r
     centre pressures.  Inverses are assembled and factorised on the GPU
     (K7) unless ``factor=False`` (then ``set_inverses`` must be called).
+
+    ``mode``: "full" stores each patch's (s b)^2 inverse (the reference's
+    formulation); "kron" the Butcher eigen-split (s b^2 doubles per patch,
+    3x fewer bytes at s = 3); "auto" picks "kron" when all stages share the
+    convection Jacobian, A is well diagonalisable and b <= 64.
     """
 
-    def __init__(self, system, mesh, omega=1.0, factor=True):
+    def __init__(self, system, mesh, omega=1.0, factor=True, mode="auto"):
         self.omega = float(omega)
         self.system = system
         self.num_patches = mesh.num_vertices
         self.tables = build_patch_tables(mesh, system.n_nodes, system.n_p, system.r,
                                          system.node_constrained)
+        if mode not in ("auto", "full", "kron"):
+            raise ValueError(f"unknown patch mode {mode!r}")
+        self.kron = None
+        if mode in ("auto", "kron"):
+            try:
+                shared = system.convection is None or len(system._conv_vals) == 1
+                if not shared:
+                    raise ValueError("per-stage convection Jacobians differ")
+                if self.tables.max_m // system.r > 64:
+                    raise ValueError("patch block too large for the kron kernels")
+                self.kron = KronSplit(system.tableau.A)
+            except ValueError:
+                if mode == "kron":
+                    raise
+                self.kron = None
+        self.mode = "kron" if self.kron is not None else "full"
+        self._layout()
         self._dev = None
         self._factored = False
         if factor:
             self.factor()
+
+    def _layout(self):
+        t = self.tables
+        if self.kron is None:
+            self.inv_off, self.inv_size = t.inv_off, t.inv_size
+        else:
+            sizes = np.array([self.kron.block_doubles(int(m) // t.stages) for m in t.sizes],
+                             dtype=np.int64)
+            off = np.concatenate([[0], np.cumsum(sizes)])
+            self.inv_off, self.inv_size = off[:-1], int(off[-1])
 
     # -- reference attributes ------------------------------------------------
 
@@ -140,11 +239,30 @@ class VankaPatchSet:
         inv_all = dev["inv"]
         out = []
         for m, first, count in t.groups():
-            ld = (m + 3) & ~3
-            off = int(t.inv_off[first])
-            blk = inv_all[off:off + count * m * ld].view(count, m, ld)[:, :, :m]
-            inv = blk.transpose(1, 2).contiguous().cpu().numpy()
             idx = t.idx[t.idx_off[first]:t.idx_off[first + count]].reshape(count, m)
+            off = int(self.inv_off[first])
+            if self.kron is None:
+                ld = (m + 3) & ~3
+                blk = inv_all[off:off + count * m * ld].view(count, m, ld)[:, :, :m]
+                inv = blk.transpose(1, 2).contiguous().cpu().numpy()
+            else:
+                b = m // t.stages
+                per = self.kron.block_doubles(b)
+                raw = inv_all[off:off + count * per].view(count, per).cpu().numpy()
+                inv = np.empty((count, m, m))
+                for q in range(count):
+                    G, pos = [], 0
+                    for cplx in self.kron.is_complex:
+                        if cplx:
+                            ldc = (b + 1) & ~1
+                            a = raw[q, pos:pos + 2 * b * ldc].reshape(b, ldc, 2)[:, :b]
+                            G.append((a[..., 0] + 1j * a[..., 1]).T)
+                            pos += 2 * b * ldc
+                        else:
+                            ldr = (b + 3) & ~3
+                            G.append(raw[q, pos:pos + b * ldr].reshape(b, ldr)[:, :b].T)
+                            pos += b * ldr
+                    inv[q] = self.kron.full_inverse(G, b)
             out.append((idx.copy(), inv))
         return out
 
@@ -173,8 +291,8 @@ class VankaPatchSet:
         d = {}
         d["idx_off"] = upload(t.idx_off, np.int32)
         d["idx"] = upload(t.idx, np.int32)
-        d["inv_off"] = upload(t.inv_off, np.int64)
-        d["inv"] = torch.zeros(t.inv_size, dtype=torch.float64, device=d["idx"].device)
+        d["inv_off"] = upload(self.inv_off, np.int64)
+        d["inv"] = torch.zeros(self.inv_size, dtype=torch.float64, device=d["idx"].device)
         d["dof_ptr"] = upload(t.dof_ptr, np.int32)
         d["dof_pos"] = upload(t.dof_pos, np.int32)
         d["vertex"] = upload(t.order, np.int32)
@@ -190,6 +308,9 @@ class VankaPatchSet:
         for name in ("idx_off", "idx", "inv_off", "inv", "dof_ptr", "dof_pos", "vertex",
                      "node_off", "node"):
             setattr(desc, name, d[name].data_ptr())
+        if self.kron is not None:
+            d["kron"] = self.kron.desc()          # keep the host struct alive
+            desc.kron = C.pointer(d["kron"])
         d["desc"] = desc
         self._dev = d
         return d
@@ -216,6 +337,11 @@ class VankaPatchSet:
         format [(idx (P,m), inv (P,m,m))] instead of factorising on the GPU."""
         import torch
         t = self.tables
+        if self.kron is not None:       # reference inverses are full (s b)^2 blocks
+            self.kron = None
+            self.mode = "full"
+            self._layout()
+            self._dev = None
         dev = self.device_data()
         mine = t.groups()
         if len(groups) != len(mine):

@@ -25,7 +25,7 @@ WELL_CONDITIONED = {"cfg1", "ns", "crossed"}
 
 
 class Case:
-    def __init__(self, name):
+    def __init__(self, name, mode):
         import torch
         from paper_2202_07381_b200 import MGHierarchyOp, MGLevel, SmootherSpec
         self.name = name
@@ -33,7 +33,10 @@ class Case:
         self.disc, self.tab, self.conv, self.case = setup(name)
         c = self.case
         cheb = SmootherSpec(pre=2, post=2, accel="chebyshev", cheby_a=c["cheby_a"], cheby_b=8.0)
-        self.mg, self.S = self.disc.build_mg(self.tab, c["dt"], cheb, convection=self.conv)
+        self.mode = mode
+        self.mg, self.S = self.disc.build_mg(self.tab, c["dt"], cheb, convection=self.conv,
+                                             patch_mode=mode)
+        assert self.mg.levels[-1].patches.mode == mode
         pou = SmootherSpec(pre=2, post=2, accel="richardson", omega=0.5, weighting="pou")
         self.mg_pou = MGHierarchyOp([MGLevel(l.system, l.patches, pou, l.prolong)
                                      for l in self.mg.levels], self.mg.coarse)
@@ -44,10 +47,12 @@ class Case:
 _cache = {}
 
 
-@pytest.fixture(params=CASES)
+@pytest.fixture(params=[(n, m) for n in CASES for m in ("kron", "full")],
+                ids=lambda p: f"{p[0]}-{p[1]}")
 def case(request):
     if request.param not in _cache:
-        _cache[request.param] = Case(request.param)
+        _cache.clear()   # one case resident at a time
+        _cache[request.param] = Case(*request.param)
     return _cache[request.param]
 
 
