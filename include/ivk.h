@@ -63,6 +63,21 @@ typedef struct ivk_operator_desc {
   const int32_t* bt_col;    /* nnz_b (scalar P2 node)                      */
   const double* bt_val;     /* nnz_b * 2                                   */
   const uint8_t* node_constrained; /* n_nodes: 1 = both components fixed   */
+  /* The same operator in sliced-ELL form for the K1 apply: velocity rows
+   * (p2_*, conv_s, b_*) in SELL-16, pressure rows (bt_*) in SELL-32; entry
+   * e of a slice's j-th row at ptr[slice] + H e + j, padding entries carry
+   * zero values.  The CSR arrays above serve the patch assembly (K7). */
+  const int32_t* p2_sptr;   /* ceil(n_nodes/16) + 1                        */
+  const int32_t* p2_scol;
+  const double* p2_smk;     /* (m, k) per entry                            */
+  const double* conv_s;     /* n_conv blocks of (Jxx, Jxy, Jyx, Jyy)       */
+  int32_t nnz_s;            /* SELL entries per operand (conv stride)      */
+  const int32_t* b_sptr;
+  const int32_t* b_scol;
+  const double* b_sval;
+  const int32_t* bt_sptr;   /* ceil(n_p/32) + 1                            */
+  const int32_t* bt_scol;
+  const double* bt_sval;
 } ivk_operator_desc;
 
 /* Vanka vertex-star patch set (solvers.py:116-222).  Patches are laid out
@@ -86,6 +101,10 @@ typedef struct ivk_patch_desc {
   const int32_t* vertex;   /* num_patches: centre vertex                  */
   const int32_t* node_off; /* num_patches + 1                             */
   const int32_t* node;     /* free scalar P2 nodes of each patch, sorted  */
+  const int32_t* slot_pos; /* total_m or NULL: where patch slot k is written
+                              in local[] (owner-sorted, so the scatter reads
+                              local[dof_ptr[d] .. dof_ptr[d+1]) contiguously);
+                              NULL = patch order, scatter gathers via dof_pos */
   const struct ivk_kron_desc* kron; /* HOST pointer; NULL = full inverses */
 } ivk_patch_desc;
 
@@ -135,6 +154,7 @@ typedef struct ivk_transfer_desc {
 typedef struct ivk_coarse_desc {
   int32_t n;               /* = stages * (n_u + n_p)                      */
   int32_t nb;              /* ceil(n / 32) block columns                  */
+  int32_t l_ntiles, u_ntiles; /* off-diagonal tile counts                 */
   int32_t stages, n_u, n_p;
   const int32_t* l_colptr; /* nb + 1                                      */
   const int32_t* l_row;    /* block row I of each off-diagonal L tile     */
@@ -159,12 +179,13 @@ int64_t ivk_launch_count(void);
 int ivk_stage_apply(const ivk_operator_desc* op, const double* x, const double* b,
                     double* out, void* stream);
 
-/* local[idx_off[p] + i] = sum_j Inv_p[i][j] * r[idx[idx_off[p] + j]]
+/* local[slot_pos[idx_off[p] + i]] = sum_j Inv_p[i][j] * r[idx[idx_off[p] + j]]
  * (gather + batched patch solve: einsum at solvers.py:219-220). */
 int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, void* stream);
 
 /* Deterministic scatter (bincount at solvers.py:221) fused with the update:
- * z_d = sum over dof_pos of local; out_d = alpha * x_d + beta * w_d * z_d
+ * z_d = sum_{k = dof_ptr[d]}^{dof_ptr[d+1]-1} local[k] (contributions in the
+ * reference's group/patch order); out_d = alpha * x_d + beta * w_d * z_d
  * (x == NULL -> 0, w == NULL -> 1); if accum != NULL also accum_d += out_d.
  * out may alias x. */
 int ivk_patch_combine(const ivk_patch_desc* pd, const double* local, const double* x,

@@ -40,6 +40,10 @@ class OperatorDesc(C.Structure):
         ("b_rowptr", C.c_void_p), ("b_col", C.c_void_p), ("b_val", C.c_void_p),
         ("bt_rowptr", C.c_void_p), ("bt_col", C.c_void_p), ("bt_val", C.c_void_p),
         ("node_constrained", C.c_void_p),
+        ("p2_sptr", C.c_void_p), ("p2_scol", C.c_void_p), ("p2_smk", C.c_void_p),
+        ("conv_s", C.c_void_p), ("nnz_s", C.c_int32),
+        ("b_sptr", C.c_void_p), ("b_scol", C.c_void_p), ("b_sval", C.c_void_p),
+        ("bt_sptr", C.c_void_p), ("bt_scol", C.c_void_p), ("bt_sval", C.c_void_p),
     ]
 
 
@@ -63,6 +67,7 @@ class PatchDesc(C.Structure):
         ("idx_off", C.c_void_p), ("idx", C.c_void_p), ("inv_off", C.c_void_p),
         ("inv", C.c_void_p), ("dof_ptr", C.c_void_p), ("dof_pos", C.c_void_p),
         ("vertex", C.c_void_p), ("node_off", C.c_void_p), ("node", C.c_void_p),
+        ("slot_pos", C.c_void_p),
         ("kron", C.POINTER(KronDesc)),
     ]
 
@@ -81,8 +86,8 @@ class TransferDesc(C.Structure):
 
 class CoarseDesc(C.Structure):
     _fields_ = [
-        ("n", C.c_int32), ("nb", C.c_int32), ("stages", C.c_int32), ("n_u", C.c_int32),
-        ("n_p", C.c_int32),
+        ("n", C.c_int32), ("nb", C.c_int32), ("l_ntiles", C.c_int32), ("u_ntiles", C.c_int32),
+        ("stages", C.c_int32), ("n_u", C.c_int32), ("n_p", C.c_int32),
         ("l_colptr", C.c_void_p), ("l_row", C.c_void_p), ("l_tiles", C.c_void_p),
         ("l_diag", C.c_void_p),
         ("u_colptr", C.c_void_p), ("u_row", C.c_void_p), ("u_tiles", C.c_void_p),

@@ -8,11 +8,13 @@
 //
 // Tile-sparse blocked substitution: the factors are stored as 32 x 32 tiles
 // (column-major), only the ~1/3 nonzero ones.  Per block column K one warp
-// solves the diagonal tile with register shuffles while the other 15 warps
-// hold the (already prefetched) off-diagonal tiles of column K in registers
-// and apply the rank-32 update as soon as y_K is published; each warp then
-// prefetches its tile of column K+1, so the L2 latency is off the critical
-// path (2 CTA barriers per block column).
+// solves the diagonal tile with register shuffles, its tiles streamed two
+// steps ahead into a shared-memory ring by TMA bulk copies (cp.async.bulk +
+// mbarrier); the other 15 warps hold the (already prefetched) off-diagonal
+// tiles of column K in registers and apply the rank-32 update as soon as y_K
+// is published, then prefetch their tile of column K+1.  Tile metadata is
+// staged in shared memory, so no global load sits on the critical path
+// (2 CTA barriers per block column).
 
 #include "ivk_common.cuh"
 
@@ -73,57 +75,118 @@ __device__ __forceinline__ void load_tile(double (&t)[32], const double* __restr
   for (int jj = 0; jj < 32; ++jj) t[jj] = __ldg(tile + jj * 32 + lane);
 }
 
+// ---- TMA bulk copies of the diagonal tiles into a shared-memory ring ------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  // the slot was last read through the generic proxy (before a CTA barrier)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kDiagRing = 3;  // diagonal tiles in flight (TMA), 2 steps ahead
+
+// One triangular solve.  colptr / rowtile live in shared memory; the diagonal
+// tiles stream through a 3-slot TMA ring; each tile warp keeps its next
+// off-diagonal tile in registers.
 template <bool LOWER>
-__device__ void tile_solve(int nb, const int32_t* __restrict__ colptr,
-                           const int32_t* __restrict__ rowtile, const double* __restrict__ tiles,
-                           const double* __restrict__ diag, double* y) {
+__device__ void tile_solve(int nb, const int32_t* colptr, const int32_t* rowtile,
+                           const double* __restrict__ tiles, const double* __restrict__ diag,
+                           double* y, double* ring, uint64_t* bars, uint32_t& phase_bits) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int step = LOWER ? 1 : -1;
-  int K = LOWER ? 0 : nb - 1;
+  const int K0 = LOWER ? 0 : nb - 1;
   double t[32];
-  if (warp == kDiagWarp) {
-    load_tile(t, diag + (long)K * 1024, lane);
-  } else {
-    const int ti = colptr[K] + warp;
-    if (ti < colptr[K + 1]) load_tile(t, tiles + (long)ti * 1024, lane);
+  if (warp == kDiagWarp && lane == 0) {
+    for (int s = 0; s < kDiagRing - 1 && s < nb; ++s)
+      bulk_load(ring + s * 1024, diag + (long)(K0 + s * step) * 1024, 8192, &bars[s]);
   }
+  if (warp < kTileWarps) {
+    const int ti = colptr[K0] + warp;
+    if (ti < colptr[K0 + 1]) load_tile(t, tiles + (long)ti * 1024, lane);
+  }
+  int K = K0;
   for (int s = 0; s < nb; ++s, K += step) {
     if (warp == kDiagWarp) {
+      const int slot = s % kDiagRing;
+      if (lane == 0 && s + kDiagRing - 1 < nb) {
+        const int ns = (s + kDiagRing - 1) % kDiagRing;
+        bulk_load(ring + ns * 1024, diag + (long)(K + (kDiagRing - 1) * step) * 1024, 8192,
+                  &bars[ns]);
+      }
+      mbar_wait(&bars[slot], (phase_bits >> slot) & 1u);
+      const double* D = ring + slot * 1024;
       double yl = y[K * 32 + lane];
       if (LOWER) {
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
+          const double d = D[jj * 32 + lane];
           const double yj = __shfl_sync(0xffffffffu, yl, jj);
-          if (lane > jj) yl = fma(-t[jj], yj, yl);
+          if (lane > jj) yl = fma(-d, yj, yl);
         }
       } else {
+        // the diagonal slot of an upper tile holds 1 / U_jj (tile_factor)
 #pragma unroll
         for (int jj = 31; jj >= 0; --jj) {
-          if (lane == jj) yl = yl / t[jj];
+          const double d = D[jj * 32 + lane];
+          if (lane == jj) yl = yl * d;
           const double yj = __shfl_sync(0xffffffffu, yl, jj);
-          if (lane < jj) yl = fma(-t[jj], yj, yl);
+          if (lane < jj) yl = fma(-d, yj, yl);
         }
       }
       y[K * 32 + lane] = yl;
-      if (s + 1 < nb) load_tile(t, diag + (long)(K + step) * 1024, lane);
     }
+    // every thread flips its copy of the slot parity (uniform bookkeeping)
+    phase_bits ^= 1u << (s % kDiagRing);
     __syncthreads();
     if (warp < kTileWarps) {
       const int c0 = colptr[K], c1 = colptr[K + 1];
       const double* yk = y + K * 32;
       int ti = c0 + warp;
       if (ti < c1) {
-        double acc = 0.0;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) acc = fma(t[jj], yk[jj], acc);
-        y[rowtile[ti] * 32 + lane] -= acc;
+        for (int jj = 0; jj < 32; jj += 4) {
+          a0 = fma(t[jj], yk[jj], a0);
+          a1 = fma(t[jj + 1], yk[jj + 1], a1);
+          a2 = fma(t[jj + 2], yk[jj + 2], a2);
+          a3 = fma(t[jj + 3], yk[jj + 3], a3);
+        }
+        y[rowtile[ti] * 32 + lane] -= (a0 + a1) + (a2 + a3);
       }
       for (ti += kTileWarps; ti < c1; ti += kTileWarps) {
-        const double* tile = tiles + (long)ti * 1024;
-        double acc = 0.0;
-#pragma unroll 8
-        for (int jj = 0; jj < 32; ++jj) acc = fma(__ldg(tile + jj * 32 + lane), yk[jj], acc);
-        y[rowtile[ti] * 32 + lane] -= acc;
+        double u[32];
+        load_tile(u, tiles + (long)ti * 1024, lane);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 4) {
+          a0 = fma(u[jj], yk[jj], a0);
+          a1 = fma(u[jj + 1], yk[jj + 1], a1);
+          a2 = fma(u[jj + 2], yk[jj + 2], a2);
+          a3 = fma(u[jj + 3], yk[jj + 3], a3);
+        }
+        y[rowtile[ti] * 32 + lane] -= (a0 + a1) + (a2 + a3);
       }
       if (s + 1 < nb) {
         const int Kn = K + step;
@@ -138,11 +201,29 @@ __device__ void tile_solve(int nb, const int32_t* __restrict__ colptr,
 __global__ void __launch_bounds__(kCoarseThreads, 1) coarse_solve_kernel(CoarseParams c,
                                                                          const double* __restrict__ b,
                                                                          double* __restrict__ x) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(128) double sm[];
   const int npad = c.nb * 32;
-  double* v = sm;         // npad
-  double* y = sm + npad;  // npad
+  const int nl = c.l_colptr[c.nb], nu_t = c.u_colptr[c.nb];
+  double* ring = sm;                       // kDiagRing tiles (TMA destination)
+  double* v = ring + kDiagRing * 1024;     // npad
+  double* y = v + npad;                    // npad
+  int32_t* meta = reinterpret_cast<int32_t*>(y + npad);
+  int32_t* lcol = meta;                    // nb + 1
+  int32_t* lrow = lcol + c.nb + 1;         // nl
+  int32_t* ucol = lrow + nl;               // nb + 1
+  int32_t* urow = ucol + c.nb + 1;         // nu_t
   __shared__ double red[32];
+  __shared__ __align__(8) uint64_t bars[kDiagRing];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kDiagRing; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i <= c.nb; i += blockDim.x) {
+    lcol[i] = c.l_colptr[i];
+    ucol[i] = c.u_colptr[i];
+  }
+  for (int i = threadIdx.x; i < nl; i += blockDim.x) lrow[i] = c.l_row[i];
+  for (int i = threadIdx.x; i < nu_t; i += blockDim.x) urow[i] = c.u_row[i];
   for (int i = threadIdx.x; i < npad; i += blockDim.x) {
     v[i] = i < c.n ? b[i] : 0.0;
     y[i] = 0.0;
@@ -151,8 +232,9 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) coarse_solve_kernel(CoarseP
   project_smem(v, c.S, c.n_u, c.n_p, red);
   for (int i = threadIdx.x; i < c.n; i += blockDim.x) y[c.perm_r[i]] = v[i];
   __syncthreads();
-  tile_solve<true>(c.nb, c.l_colptr, c.l_row, c.l_tiles, c.l_diag, y);
-  tile_solve<false>(c.nb, c.u_colptr, c.u_row, c.u_tiles, c.u_diag, y);
+  uint32_t phase_bits = 0;
+  tile_solve<true>(c.nb, lcol, lrow, c.l_tiles, c.l_diag, y, ring, bars, phase_bits);
+  tile_solve<false>(c.nb, ucol, urow, c.u_tiles, c.u_diag, y, ring, bars, phase_bits);
   for (int i = threadIdx.x; i < c.n; i += blockDim.x) v[i] = y[c.perm_c[i]];
   __syncthreads();
   project_smem(v, c.S, c.n_u, c.n_p, red);
@@ -172,7 +254,9 @@ int ivk_coarse_solve(const ivk_coarse_desc* c, const double* b, double* x, void*
   IVK_REQUIRE(b && x && b != x, "bad coarse vectors");
   IVK_REQUIRE(c->n == c->stages * (c->n_u + c->n_p) && c->n > 0, "coarse dimension mismatch");
   IVK_REQUIRE(c->nb * 32 >= c->n && (c->nb - 1) * 32 < c->n, "coarse block count mismatch");
-  const size_t smem = 2 * (size_t)c->nb * 32 * sizeof(double);
+  IVK_REQUIRE(c->l_ntiles >= 0 && c->u_ntiles >= 0, "bad tile counts");
+  const size_t smem = (size_t)kDiagRing * 8192 + 2 * (size_t)c->nb * 32 * sizeof(double) +
+                      (size_t)(2 * (c->nb + 1) + c->l_ntiles + c->u_ntiles) * sizeof(int32_t);
   if (smem > 200 * 1024) {
     set_error("ivk_coarse_solve: coarse dimension %d too large for one CTA", c->n);
     return IVK_EUNSUPPORTED;

@@ -37,135 +37,136 @@ int check_launch(const char* what) {
 // Everything the operator kernel needs, passed by value (kernel parameter
 // space), so no device-side descriptor copy is required.
 struct OpParams {
-  int n_nodes, n_p, n_conv, nnz;
+  int n_nodes, n_p, n_conv, nnz_s;
   double dt;
   double a[IVK_MAX_STAGES * IVK_MAX_STAGES];
-  const int32_t* __restrict__ p2_rowptr;
-  const int32_t* __restrict__ p2_col;
-  const double2* __restrict__ p2_mk;
-  const double4* __restrict__ conv;
-  const int32_t* __restrict__ b_rowptr;
-  const int32_t* __restrict__ b_col;
-  const double2* __restrict__ b_val;
-  const int32_t* __restrict__ bt_rowptr;
-  const int32_t* __restrict__ bt_col;
-  const double2* __restrict__ bt_val;
+  const int32_t* __restrict__ p2_sptr;
+  const int32_t* __restrict__ p2_scol;
+  const double2* __restrict__ p2_smk;
+  const double4* __restrict__ conv_s;
+  const int32_t* __restrict__ b_sptr;
+  const int32_t* __restrict__ b_scol;
+  const double2* __restrict__ b_sval;
+  const int32_t* __restrict__ bt_sptr;
+  const int32_t* __restrict__ bt_scol;
+  const double2* __restrict__ bt_sval;
   const uint8_t* __restrict__ cmask;
 };
 
-// One thread per scalar P2 node (both components, all S stages), then one
-// thread per P1 node.  NC = 0 (Stokes), 1 (one J shared by all stages) or
-// S (per-stage J_i).
+// Velocity rows: SELL-16, one warp per 16-row slice, lane = 2 * row + comp
+// (each thread one velocity component of one node, all S stages; the lane
+// pair shares the entry's col / (m,k) loads, its x gathers hit one sector).
+// Pressure rows: SELL-32, one thread per P1 node.  Entry e of a slice's
+// row j sits at ptr[slice] + H e + j (H = 16 / 32).
+// NC = 0 (Stokes), 1 (one J shared by all stages) or S (per-stage J_i).
 template <int S, int NC>
 __global__ void __launch_bounds__(256) stage_apply_kernel(OpParams op, const double* __restrict__ x,
                                                           const double* __restrict__ b,
                                                           double* __restrict__ out) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nslice_v = (op.n_nodes + 15) >> 4;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   const int nu = 2 * op.n_nodes;
   const long sd = nu + op.n_p;
-  if (row < op.n_nodes) {
-    const int n = row;
-    if (op.cmask[n]) {
+  if (warp < nslice_v) {
+    const int j = lane >> 1, c = lane & 1;
+    const int n = (warp << 4) + j;
+    const bool valid = n < op.n_nodes;
+    const bool fixed = valid && op.cmask[n];
+    double mu[S], ku[S], ju[(NC > 1) ? S : 1];
 #pragma unroll
-      for (int t = 0; t < S; ++t) {
-        const long o = t * sd + 2 * n;
-        const double y0 = x[o], y1 = x[o + 1];
-        out[o] = b ? b[o] - y0 : y0;
-        out[o + 1] = b ? b[o + 1] - y1 : y1;
-      }
-      return;
-    }
-    double mu[S][2], ku[S][2], bp[S][2], ju[S][2];
+    for (int t = 0; t < S; ++t) mu[t] = ku[t] = 0.0;
 #pragma unroll
-    for (int t = 0; t < S; ++t)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) mu[t][c] = ku[t][c] = bp[t][c] = ju[t][c] = 0.0;
-
-    const int e0 = op.p2_rowptr[n], e1 = op.p2_rowptr[n + 1];
-    for (int e = e0; e < e1; ++e) {
-      const int col = op.p2_col[e];
-      const double2 mk = op.p2_mk[e];
-      double ux[S], uy[S];
-#pragma unroll
-      for (int t = 0; t < S; ++t) {
-        ux[t] = x[t * sd + 2 * col];
-        uy[t] = x[t * sd + 2 * col + 1];
-        mu[t][0] = fma(mk.x, ux[t], mu[t][0]);
-        mu[t][1] = fma(mk.x, uy[t], mu[t][1]);
-        ku[t][0] = fma(mk.y, ux[t], ku[t][0]);
-        ku[t][1] = fma(mk.y, uy[t], ku[t][1]);
-      }
-      if constexpr (NC == 1) {
-        const double4 J = op.conv[e];
+    for (int t = 0; t < ((NC > 1) ? S : 1); ++t) ju[t] = 0.0;
+    if (!fixed) {
+      const int e0 = op.p2_sptr[warp], e1 = op.p2_sptr[warp + 1];
+#pragma unroll 2
+      for (int e = e0 + j; e < e1; e += 16) {
+        const int col = op.p2_scol[e];
+        const double2 mk = op.p2_smk[e];
+        double u[S];
 #pragma unroll
         for (int t = 0; t < S; ++t) {
-          ju[t][0] += J.x * ux[t] + J.y * uy[t];
-          ju[t][1] += J.z * ux[t] + J.w * uy[t];
+          u[t] = x[t * sd + 2 * col + c];
+          mu[t] = fma(mk.x, u[t], mu[t]);
+          ku[t] = fma(mk.y, u[t], ku[t]);
         }
-      } else if constexpr (NC == S && NC > 1) {
-        // Row stage i uses J_i applied to sum_j a_ij u_j (stages.py:118-123).
+        if constexpr (NC >= 1) {
+          // the other component of the same node (J couples components)
+          double v[S];
 #pragma unroll
-        for (int i = 0; i < S; ++i) {
-          const double4 J = op.conv[(long)i * op.nnz + e];
-          double wx = 0.0, wy = 0.0;
+          for (int t = 0; t < S; ++t) v[t] = x[t * sd + 2 * col + (c ^ 1)];
+          if constexpr (NC == 1) {
+            const double4 J = op.conv_s[e];
+            const double jd = c ? J.w : J.x, jo = c ? J.z : J.y;  // row c: own, other
 #pragma unroll
-          for (int j = 0; j < S; ++j) {
-            wx += op.a[i * S + j] * ux[j];
-            wy += op.a[i * S + j] * uy[j];
+            for (int t = 0; t < S; ++t) ku[t] += jd * u[t] + jo * v[t];
+          } else {
+            // Row stage i uses J_i applied to sum_j a_ij u_j (stages.py:118-123).
+#pragma unroll
+            for (int i = 0; i < S; ++i) {
+              const double4 J = op.conv_s[(long)i * op.nnz_s + e];
+              const double jd = c ? J.w : J.x, jo = c ? J.z : J.y;
+              double wu = 0.0, wv = 0.0;
+#pragma unroll
+              for (int t = 0; t < S; ++t) {
+                wu += op.a[i * S + t] * u[t];
+                wv += op.a[i * S + t] * v[t];
+              }
+              ju[i] += jd * wu + jo * wv;
+            }
           }
-          ju[i][0] += J.x * wx + J.y * wy;
-          ju[i][1] += J.z * wx + J.w * wy;
         }
       }
-    }
-    const int f0 = op.b_rowptr[n], f1 = op.b_rowptr[n + 1];
-    for (int e = f0; e < f1; ++e) {
-      const int q = op.b_col[e];
-      const double2 bv = op.b_val[e];
+      const int f0 = op.b_sptr[warp], f1 = op.b_sptr[warp + 1];
+      for (int e = f0 + j; e < f1; e += 16) {
+        const int q = op.b_scol[e];
+        const double2 bv = op.b_sval[e];
+        const double bc = c ? bv.y : bv.x;
 #pragma unroll
-      for (int t = 0; t < S; ++t) {
-        const double p = x[t * sd + nu + q];
-        bp[t][0] = fma(bv.x, p, bp[t][0]);
-        bp[t][1] = fma(bv.y, p, bp[t][1]);
+        for (int t = 0; t < S; ++t) ku[t] = fma(bc, x[t * sd + nu + q], ku[t]);
       }
     }
+    if (!valid) return;
 #pragma unroll
     for (int i = 0; i < S; ++i) {
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      const long o = i * sd + 2 * n + c;
+      double y;
+      if (fixed) {
+        y = x[o];
+      } else {
         double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < S; ++j) {
-          double kj = ku[j][c] + bp[j][c];
-          if constexpr (NC == 1) kj += ju[j][c];
-          acc += op.a[i * S + j] * kj;
-        }
-        double y = mu[i][c] + op.dt * acc;
-        if constexpr (NC == S && NC > 1) y += op.dt * ju[i][c];
-        const long o = i * sd + 2 * n + c;
-        out[o] = b ? b[o] - y : y;
+        for (int t = 0; t < S; ++t) acc += op.a[i * S + t] * ku[t];
+        y = mu[i] + op.dt * acc;
+        if constexpr (NC > 1) y += op.dt * ju[i];
       }
+      out[o] = b ? b[o] - y : y;
     }
-  } else if (row < op.n_nodes + op.n_p) {
-    const int q = row - op.n_nodes;
+  } else {
+    const int ws = warp - nslice_v;
+    const int q = (ws << 5) + lane;
+    if (ws >= ((op.n_p + 31) >> 5)) return;
     double btu[S];
 #pragma unroll
     for (int t = 0; t < S; ++t) btu[t] = 0.0;
-    const int e0 = op.bt_rowptr[q], e1 = op.bt_rowptr[q + 1];
-    for (int e = e0; e < e1; ++e) {
-      const int n = op.bt_col[e];
-      const double2 bv = op.bt_val[e];
+    const int e0 = op.bt_sptr[ws], e1 = op.bt_sptr[ws + 1];
+#pragma unroll 2
+    for (int e = e0 + lane; e < e1; e += 32) {
+      const int n = op.bt_scol[e];
+      const double2 bv = op.bt_sval[e];
 #pragma unroll
       for (int t = 0; t < S; ++t) {
         btu[t] = fma(bv.x, x[t * sd + 2 * n], btu[t]);
         btu[t] = fma(bv.y, x[t * sd + 2 * n + 1], btu[t]);
       }
     }
+    if (q >= op.n_p) return;
 #pragma unroll
     for (int i = 0; i < S; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < S; ++j) acc += op.a[i * S + j] * btu[j];
+      for (int t = 0; t < S; ++t) acc += op.a[i * S + t] * btu[t];
       const double y = op.dt * acc;
       const long o = i * sd + nu + q;
       out[o] = b ? b[o] - y : y;
@@ -179,19 +180,19 @@ OpParams make_op_params(const ivk_operator_desc* d) {
   p.n_nodes = d->n_nodes;
   p.n_p = d->n_p;
   p.n_conv = d->n_conv;
-  p.nnz = d->nnz;
+  p.nnz_s = d->nnz_s;
   p.dt = d->dt;
   for (int i = 0; i < IVK_MAX_STAGES * IVK_MAX_STAGES; ++i) p.a[i] = d->butcher_a[i];
-  p.p2_rowptr = d->p2_rowptr;
-  p.p2_col = d->p2_col;
-  p.p2_mk = reinterpret_cast<const double2*>(d->p2_mk);
-  p.conv = reinterpret_cast<const double4*>(d->conv);
-  p.b_rowptr = d->b_rowptr;
-  p.b_col = d->b_col;
-  p.b_val = reinterpret_cast<const double2*>(d->b_val);
-  p.bt_rowptr = d->bt_rowptr;
-  p.bt_col = d->bt_col;
-  p.bt_val = reinterpret_cast<const double2*>(d->bt_val);
+  p.p2_sptr = d->p2_sptr;
+  p.p2_scol = d->p2_scol;
+  p.p2_smk = reinterpret_cast<const double2*>(d->p2_smk);
+  p.conv_s = reinterpret_cast<const double4*>(d->conv_s);
+  p.b_sptr = d->b_sptr;
+  p.b_scol = d->b_scol;
+  p.b_sval = reinterpret_cast<const double2*>(d->b_sval);
+  p.bt_sptr = d->bt_sptr;
+  p.bt_scol = d->bt_scol;
+  p.bt_sval = reinterpret_cast<const double2*>(d->bt_sval);
   p.cmask = d->node_constrained;
   return p;
 }
@@ -208,6 +209,10 @@ int validate_op(const ivk_operator_desc* d) {
   IVK_REQUIRE(d->p2_rowptr && d->p2_col && d->p2_mk && d->b_rowptr && d->b_col && d->b_val &&
                   d->bt_rowptr && d->bt_col && d->bt_val && d->node_constrained,
               "operator descriptor has a NULL array");
+  IVK_REQUIRE(d->p2_sptr && d->p2_scol && d->p2_smk && d->b_sptr && d->b_scol && d->b_sval &&
+                  d->bt_sptr && d->bt_scol && d->bt_sval,
+              "operator descriptor has a NULL SELL array");
+  IVK_REQUIRE(d->n_conv == 0 || d->conv_s != nullptr, "conv_s is NULL with n_conv > 0");
   return IVK_OK;
 }
 
@@ -215,9 +220,9 @@ template <int S>
 static void launch_stage_apply(const OpParams& q, int nconv, const double* x, const double* b,
                                double* out, cudaStream_t st) {
   const OpParams& p = q;
-  const int rows = p.n_nodes + p.n_p;
+  const long warps = ((p.n_nodes + 15) >> 4) + ((p.n_p + 31) >> 5);
   const int block = 256;
-  const int grid = (rows + block - 1) / block;
+  const int grid = (int)((warps * 32 + block - 1) / block);
   if (nconv == 0)
     stage_apply_kernel<S, 0><<<grid, block, 0, st>>>(q, x, b, out);
   else if (nconv == 1)

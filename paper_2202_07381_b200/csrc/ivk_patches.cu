@@ -31,6 +31,7 @@ struct PatchParams {
   const int32_t* __restrict__ vertex;
   const int32_t* __restrict__ node_off;
   const int32_t* __restrict__ node;
+  const int32_t* __restrict__ slot_pos;
 };
 
 static PatchParams make_patch_params(const ivk_patch_desc* d) {
@@ -48,13 +49,15 @@ static PatchParams make_patch_params(const ivk_patch_desc* d) {
   p.vertex = d->vertex;
   p.node_off = d->node_off;
   p.node = d->node;
+  p.slot_pos = d->slot_pos;
   return p;
 }
 
 static int validate_patches(const ivk_patch_desc* d) {
   IVK_REQUIRE(d != nullptr, "patch descriptor is NULL");
   IVK_REQUIRE(d->num_patches > 0 && d->dim > 0 && d->max_m > 0, "empty patch set");
-  IVK_REQUIRE(d->idx_off && d->idx && d->inv_off && d->inv && d->dof_ptr && d->dof_pos,
+  IVK_REQUIRE(d->idx_off && d->idx && d->inv_off && d->inv && d->dof_ptr &&
+                  (d->slot_pos || d->dof_pos),
               "patch descriptor has a NULL array");
   return IVK_OK;
 }
@@ -68,6 +71,15 @@ static int validate_patches(const ivk_patch_desc* d) {
 constexpr int kApplyWarps = 8;
 constexpr int kRowsPerWarp = 128;
 constexpr int kUnroll = 4;  // 4 x 32 B in flight per lane; ~48 regs -> 40 warps/SM
+
+// Patch-local results are re-read by the scatter right after: keep them in L2.
+__device__ __forceinline__ void st_keep(double* p, double v) {
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+      "st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, pol;\n\t}"
+      :: "l"(p), "d"(v) : "memory");
+}
 
 __device__ __forceinline__ void ld_stream4(const double* p, double& a, double& b, double& c,
                                            double& d) {
@@ -121,11 +133,19 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kernel(PatchPara
           acc2 = fma(v2, rj, acc2);
           acc3 = fma(v3, rj, acc3);
         }
-        double* out = local + off + i0;
-        if (i0 + 0 < m) out[0] = acc0;
-        if (i0 + 1 < m) out[1] = acc1;
-        if (i0 + 2 < m) out[2] = acc2;
-        if (i0 + 3 < m) out[3] = acc3;
+        if (pd.slot_pos) {
+          const int32_t* sp = pd.slot_pos + off + i0;
+          if (i0 + 0 < m) st_keep(local + sp[0], acc0);
+          if (i0 + 1 < m) st_keep(local + sp[1], acc1);
+          if (i0 + 2 < m) st_keep(local + sp[2], acc2);
+          if (i0 + 3 < m) st_keep(local + sp[3], acc3);
+        } else {
+          double* out = local + off + i0;
+          if (i0 + 0 < m) st_keep(out + 0, acc0);
+          if (i0 + 1 < m) st_keep(out + 1, acc1);
+          if (i0 + 2 < m) st_keep(out + 2, acc2);
+          if (i0 + 3 < m) st_keep(out + 3, acc3);
+        }
       }
     }
     __syncwarp();
@@ -140,7 +160,21 @@ __global__ void patch_combine_kernel(PatchParams pd, const double* __restrict__ 
   for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < pd.dim; d += gridDim.x * blockDim.x) {
     const int k0 = pd.dof_ptr[d], k1 = pd.dof_ptr[d + 1];
     double z = 0.0;
-    for (int k = k0; k < k1; ++k) z += local[pd.dof_pos[k]];
+    if (pd.slot_pos) {
+      for (int k = k0; k < k1; ++k) z += local[k];
+    } else {
+      int k = k0;
+      for (; k + 4 <= k1; k += 4) {
+        const int p0 = pd.dof_pos[k], p1 = pd.dof_pos[k + 1], p2 = pd.dof_pos[k + 2],
+                  p3 = pd.dof_pos[k + 3];
+        const double v0 = local[p0], v1 = local[p1], v2 = local[p2], v3 = local[p3];
+        z += v0;
+        z += v1;
+        z += v2;
+        z += v3;
+      }
+      for (; k < k1; ++k) z += local[pd.dof_pos[k]];
+    }
     double v = beta * (w ? w[d] : 1.0) * z;
     if (x) v = alpha * x[d] + v;
     out[d] = v;
@@ -682,7 +716,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_kernel(
         const double zr = rt_all[warp][k][2 * a], zi = rt_all[warp][k][2 * a + 1];
         acc += kp.scale[k] * (kp.v_re[i * S + k] * zr - kp.v_im[i * S + k] * zi);
       }
-      local[off + e] = acc;
+      st_keep(local + (pd.slot_pos ? pd.slot_pos[off + e] : off + e), acc);
     }
     __syncwarp();
   }

@@ -169,7 +169,10 @@ class VankaPatchSet:
     convection Jacobian, A is well diagonalisable and b <= 64.
     """
 
-    def __init__(self, system, mesh, omega=1.0, factor=True, mode="auto"):
+    def __init__(self, system, mesh, omega=1.0, factor=True, mode="auto", scatter="patch"):
+        if scatter not in ("patch", "owner"):
+            raise ValueError(f"unknown scatter layout {scatter!r}")
+        self.scatter = scatter
         self.omega = float(omega)
         self.system = system
         self.num_patches = mesh.num_vertices
@@ -295,6 +298,9 @@ class VankaPatchSet:
         d["inv"] = torch.zeros(self.inv_size, dtype=torch.float64, device=d["idx"].device)
         d["dof_ptr"] = upload(t.dof_ptr, np.int32)
         d["dof_pos"] = upload(t.dof_pos, np.int32)
+        slot_pos = np.empty(t.total_m, dtype=np.int64)
+        slot_pos[t.dof_pos] = np.arange(t.total_m)       # owner-sorted write position
+        d["slot_pos"] = upload(slot_pos, np.int32)
         d["vertex"] = upload(t.order, np.int32)
         d["node_off"] = upload(t.node_off, np.int32)
         d["node"] = upload(t.node, np.int32)
@@ -308,6 +314,7 @@ class VankaPatchSet:
         for name in ("idx_off", "idx", "inv_off", "inv", "dof_ptr", "dof_pos", "vertex",
                      "node_off", "node"):
             setattr(desc, name, d[name].data_ptr())
+        desc.slot_pos = d["slot_pos"].data_ptr() if self.scatter == "owner" else None
         if self.kron is not None:
             d["kron"] = self.kron.desc()          # keep the host struct alive
             desc.kron = C.pointer(d["kron"])
@@ -493,6 +500,7 @@ class CoarseSolver:
         d = _lib.CoarseDesc()
         d.n = s.dim
         d.nb = nb
+        d.l_ntiles, d.u_ntiles = int(lc[-1]), int(uc[-1])
         d.stages, d.n_u, d.n_p = s.r, s.n_u, s.n_p
         for k in t:
             setattr(d, k, t[k].data_ptr())
@@ -529,9 +537,14 @@ def tile_factor(F, lower, tile=32):
     bi, bj = r // tile, c // tile
     on = bi == bj
     diag[bi[on], r[on] % tile, c[on] % tile] = v[on]
-    # unit diagonal for L (implicit in SuperLU's L) and for padding rows
+    # unit diagonal for L (implicit in SuperLU's L) and for padding rows; the
+    # upper solve multiplies by the stored reciprocal of U's diagonal
     d = np.arange(npad) if lower else np.arange(n, npad)
     diag[d // tile, d % tile, d % tile] = 1.0
+    if not lower:
+        k = np.arange(nb)[:, None]
+        i = np.arange(tile)[None, :]
+        diag[k, i, i] = 1.0 / diag[k, i, i]
     off = ~on
     key = bj[off].astype(np.int64) * nb + bi[off]
     ukey, inv = np.unique(key, return_inverse=True)

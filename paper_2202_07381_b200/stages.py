@@ -15,7 +15,32 @@ import scipy.sparse as sp
 from . import _lib
 from .fem import ConvectionBlocks, StokesBlocks
 
-__all__ = ["StageSystem", "assemble_stage_operator"]
+__all__ = ["StageSystem", "assemble_stage_operator", "to_sell"]
+
+
+def to_sell(rowptr, col, vals, n_rows, pad_col=None, C=32):
+    """CSR -> SELL-C (slices of C rows, entry e of a slice's lane-th row at
+    ptr[slice] + C e + lane).  Padding entries get zero values and a valid
+    column (the row itself, or ``pad_col``)."""
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    lens = np.diff(rowptr)
+    nsl = (n_rows + C - 1) // C
+    padded = np.zeros(nsl * C, dtype=np.int64)
+    padded[:n_rows] = lens
+    width = padded.reshape(nsl, C).max(axis=1)
+    sptr = np.concatenate([[0], np.cumsum(width * C)])
+    total = int(sptr[-1])
+    rows = np.repeat(np.arange(n_rows), lens)
+    ent = np.arange(len(rows)) - rowptr[rows]
+    pos = sptr[rows // C] + ent * C + rows % C
+    fill_rows = np.repeat(np.arange(nsl * C), np.repeat(width, C))
+    scol = (np.minimum(fill_rows, n_rows - 1) if pad_col is None
+            else np.full(total, pad_col)).astype(np.int32)
+    scol[pos] = col
+    vals = np.asarray(vals)
+    sval = np.zeros((total,) + vals.shape[1:], dtype=vals.dtype)
+    sval[pos] = vals
+    return sptr.astype(np.int32), scol, sval
 
 
 class StageSystem:
@@ -226,6 +251,23 @@ class StageSystem:
             t["conv"] = upload(np.stack(self._conv_vals).reshape(len(self._conv_vals), -1, 4),
                                np.float64)
             n_conv = len(self._conv_vals)
+        # SELL-32 copies for the K1 apply (coalesced entry loads).
+        sptr, scol, smk = to_sell(b.rowptr, b.col, np.column_stack([self._m, self._k]),
+                                  self.n_nodes, C=16)
+        t["p2_sptr"], t["p2_scol"] = upload(sptr, np.int32), upload(scol, np.int32)
+        t["p2_smk"] = upload(smk, np.float64)
+        nnz_s = len(scol)
+        if self._conv_vals is not None:
+            cs = [to_sell(b.rowptr, b.col, v.reshape(-1, 4), self.n_nodes, C=16)[2]
+                  for v in self._conv_vals]
+            t["conv_s"] = upload(np.stack(cs), np.float64)
+        sptr, scol, sval = to_sell(b.b_rowptr, b.b_col, self._b, self.n_nodes, pad_col=0, C=16)
+        t["b_sptr"], t["b_scol"], t["b_sval"] = (upload(sptr, np.int32), upload(scol, np.int32),
+                                                 upload(sval, np.float64))
+        sptr, scol, sval = to_sell(bt_rowptr, self._brows[order], self._b[order], self.n_p,
+                                   pad_col=0)
+        t["bt_sptr"], t["bt_scol"], t["bt_sval"] = (upload(sptr, np.int32), upload(scol, np.int32),
+                                                    upload(sval, np.float64))
         desc = _lib.OperatorDesc()
         desc.stages = self.r
         desc.n_nodes = self.n_nodes
@@ -248,6 +290,11 @@ class StageSystem:
         desc.bt_col = t["bt_col"].data_ptr()
         desc.bt_val = t["bt_val"].data_ptr()
         desc.node_constrained = t["cmask"].data_ptr()
+        for k in ("p2_sptr", "p2_scol", "p2_smk", "b_sptr", "b_scol", "b_sval", "bt_sptr",
+                  "bt_scol", "bt_sval"):
+            setattr(desc, k, t[k].data_ptr())
+        desc.conv_s = t["conv_s"].data_ptr() if "conv_s" in t else None
+        desc.nnz_s = nnz_s
         self._dev = {"tensors": t, "desc": desc,
                      "cmask_dofs": torch.from_numpy(self._cmask).to(t["cmask"].device)}
         return self._dev

@@ -154,7 +154,11 @@ def test_coarse_tiles_reconstruct_factors():
                 I = row[t]
                 D[I * 32:(I + 1) * 32, K * 32:(K + 1) * 32] = tiles[t * 1024:(t + 1) * 1024] \
                     .reshape(32, 32).T
-        assert np.array_equal(D[:n, :n], F.toarray())
+        Fd = F.toarray()
+        if not lower:   # the upper diagonal is stored as exact reciprocals
+            assert np.array_equal(np.diag(D)[:n], 1.0 / np.diag(Fd))
+            D[np.arange(n), np.arange(n)] = np.diag(Fd)
+        assert np.array_equal(D[:n, :n], Fd)
         assert np.array_equal(np.diag(D)[n:], np.ones(nb * 32 - n))
 
 
