@@ -29,9 +29,31 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIG = dict(name="cfg2", grid="diagonal", n0=8, level=5, mu=1.0, family="radauiia",
-              stages=3, dt=1 / 256, seed=1)
-METRIC = "IRK-Vanka fine-level sweeps/s (cfg2: 256x256 P2-P1, RadauIIA(3), dt=1/256)"
+# BASELINE.json configs 1-3 on 2-right-triangle grids with an 8x8 base.
+CONFIGS = {
+    "cfg1": dict(name="cfg1", grid="diagonal", n0=8, level=2, mu=1.0, family="radauiia",
+                 stages=2, dt=1 / 32, seed=0, cheby_a=2.0, conv=False,
+                 label="32x32 P2-P1, RadauIIA(2), dt=1/32"),
+    "cfg2": dict(name="cfg2", grid="diagonal", n0=8, level=5, mu=1.0, family="radauiia",
+                 stages=3, dt=1 / 256, seed=1, cheby_a=2.0, conv=False,
+                 label="256x256 P2-P1, RadauIIA(3), dt=1/256"),
+    "cfg3": dict(name="cfg3", grid="diagonal", n0=8, level=6, mu=0.01, family="gauss",
+                 stages=2, dt=1 / 512, seed=2, cheby_a=1.5, conv=True,
+                 label="512x512 P2-P1 Oseen Re=100, Gauss(2), dt=1/512"),
+}
+
+
+def metric_name(cfg):
+    return f"IRK-Vanka fine-level sweeps/s ({cfg['name']}: {cfg['label']})"
+
+
+def make_disc(cfg):
+    from paper_2202_07381_b200 import Discretization, tableau_lookup
+    from paper_2202_07381_b200.discretization import oseen_convection
+    disc = Discretization(cfg["n0"], cfg["level"], mu=cfg["mu"], grid=cfg["grid"])
+    tab = tableau_lookup(cfg["family"], cfg["stages"])
+    conv = oseen_convection(disc, cfg["stages"]) if cfg["conv"] else None
+    return disc, tab, conv
 
 
 def peaks():
@@ -122,19 +144,19 @@ def barrier(world):
 
 # ----------------------------------------------------------------- CPU arm
 
-def cpu_sample(sample_patches=2048, seed=CONFIG["seed"]):
+def cpu_sample(cfg, sample_patches=2048):
     """Oracle (numpy/scipy restatement of the reference) on a bounded sample
-    of the cfg2 sweep: the full-size residual matvec plus the patch solve of
-    ``sample_patches`` interior patches, extrapolated to all 66,049."""
+    of the sweep: the full-size residual matvec plus the patch solve of
+    ``sample_patches`` interior patches, extrapolated to all patches."""
     from oracle.irk_vanka_oracle import OraclePatches, OracleStageOperator, oracle_patch_indices
-    from paper_2202_07381_b200 import Discretization, tableau_lookup
     from paper_2202_07381_b200.fem import velocity_boundary_dofs
-    disc = Discretization(CONFIG["n0"], CONFIG["level"], mu=CONFIG["mu"], grid=CONFIG["grid"])
-    tab = tableau_lookup(CONFIG["family"], CONFIG["stages"])
+    disc, tab, conv = make_disc(cfg)
+    seed = cfg["seed"]
     blk = disc.blocks[-1]
     mesh = disc.fine_mesh
-    op = OracleStageOperator(blk.M, blk.K, blk.B, tab.A, CONFIG["dt"],
-                             velocity_boundary_dofs(mesh))
+    cm = None if conv is None else [J.matrix for J in conv[-1]]
+    op = OracleStageOperator(blk.M, blk.K, blk.B, tab.A, cfg["dt"],
+                             velocity_boundary_dofs(mesh), convection=cm)
     vels, idxs = oracle_patch_indices(mesh.cells, mesh.cell_to_edges, mesh.num_vertices, op)
     sizes = np.array([len(i) for i in idxs])
     interior = np.flatnonzero(sizes == sizes.max())
@@ -169,7 +191,8 @@ def time_cpu_sweep(op, pat, b, w, scale, reps=3):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    op, pat, b, w, scale, n_s, n_all = cpu_sample()
+    cfg = CONFIGS[args.config]
+    op, pat, b, w, scale, n_s, n_all = cpu_sample(cfg)
     for _ in range(args.warmup):
         time_cpu_sweep(op, pat, b, w, scale, reps=1)
     times = []
@@ -179,12 +202,12 @@ def run_reference(args, rank, world):
     t = float(np.mean(times))
     sample = (f"full-size residual matvec + patch solves of {n_s} of {n_all} interior patches "
               f"(scaled x{scale:.2f}) per step")
-    line = {"impl": "reference", "metric": METRIC, "value": 1.0 / t, "unit": "sweeps/s",
+    line = {"impl": "reference", "metric": metric_name(cfg), "value": 1.0 / t, "unit": "sweeps/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg2 fine-level IRK-Vanka sweep", "grid": "256x256 diag",
-                       "scheme": "RadauIIA(3)", "dim": op.dim},
+            "config": {"workload": f"{cfg['name']} fine-level IRK-Vanka sweep (CPU oracle port)",
+                       "problem": cfg["label"], "dim": op.dim},
             "stage_dof_updates_per_s": op.dim / t,
             "cpu_baseline": {"value": 1.0 / t, "unit": "sweeps/s", "cores": 1, "kind": "port",
                              "sample": sample},
@@ -215,21 +238,21 @@ def run_ours(args, rank, world, local):
     from paper_2202_07381_b200 import _lib
     from paper_2202_07381_b200._device import ptr, stream
 
+    cfg = CONFIGS[args.config]
     t_setup0 = time.perf_counter()
-    disc = Discretization(CONFIG["n0"], CONFIG["level"], mu=CONFIG["mu"], grid=CONFIG["grid"])
-    tab = tableau_lookup(CONFIG["family"], CONFIG["stages"])
+    disc, tab, conv = make_disc(cfg)
     t_disc = time.perf_counter() - t_setup0
-    cheb = SmootherSpec(pre=2, post=2, accel="chebyshev", cheby_a=2.0, cheby_b=8.0)
+    cheb = SmootherSpec(pre=2, post=2, accel="chebyshev", cheby_a=cfg["cheby_a"], cheby_b=8.0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    mg, S = disc.build_mg(tab, CONFIG["dt"], cheb)
+    mg, S = disc.build_mg(tab, cfg["dt"], cheb, convection=conv)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     pou = SmootherSpec(pre=2, post=2, accel="richardson", omega=0.5, weighting="pou")
     mg_pou = MGHierarchyOp([MGLevel(l.system, l.patches, pou, l.prolong) for l in mg.levels],
                            mg.coarse)
     fine = mg.levels[-1].patches
-    b_h = np.random.default_rng(CONFIG["seed"]).uniform(-1, 1, S.dim)
+    b_h = np.random.default_rng(cfg["seed"]).uniform(-1, 1, S.dim)
     b_h[S.constrained_stage_dofs()] = 0.0
     S.project_pressure_means(b_h)
     b = torch.from_numpy(b_h).cuda()
@@ -354,7 +377,7 @@ def run_ours(args, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        op, pat, bb, ww, scale, n_s, n_all = cpu_sample()
+        op, pat, bb, ww, scale, n_s, n_all = cpu_sample(cfg)
         t_cpu, t_mv, t_sa = time_cpu_sweep(op, pat, bb, ww, scale, reps=3)
         cpu = {"value": 1.0 / t_cpu, "unit": "sweeps/s", "cores": 1, "kind": "port",
                "sample": (f"oracle: full-size residual matvec ({1e3 * t_mv:.0f} ms) + patch solves "
@@ -363,16 +386,20 @@ def run_ours(args, rank, world, local):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": world / t_step, "unit": "sweeps/s", "n_gpus": world,
+            "metric": metric_name(cfg), "value": world / t_step, "unit": "sweeps/s",
+            "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded uniform[-1,1] RHS, BASELINE config 2)",
-            "config": {"workload": "cfg2 fine-level IRK-Vanka sweep (K1->K3->K4), PoU w=0.5",
-                       "patch_formulation": fine.mode,
-                       "grid": "256x256 diagonal-split, 6 levels", "scheme": "RadauIIA(3)",
-                       "dt": CONFIG["dt"], "dim": S.dim, "patches": fine.num_patches,
+            "config": {"workload": f"{cfg['name']} fine-level IRK-Vanka sweep (K1->K3->K4), "
+                                   "PoU w=0.5",
+                       "problem": cfg["label"], "patch_formulation": fine.mode,
+                       "levels": disc.num_levels, "dt": cfg["dt"], "dim": S.dim,
+                       "patches": fine.num_patches,
                        "sum_m": sm, "sum_m2": sm2,
-                       "l2": "inputs larger than L2 (7.1 GB inverse stream per step)",
+                       "l2": (f"inputs larger than L2 ({8 * fine.inv_size / 1e9:.2f} GB inverse "
+                              "stream per step)") if 8 * fine.inv_size > 126e6 else
+                             "working set fits L2 (cfg1); no flush",
                        "parallelism": f"replicas x{world}"},
             "stage_dof_updates_per_s": world * S.dim / t_step,
             "roofline": {"bound": "hbm", "kernel": f"ivk patch_apply (K2+K3, {fine.mode})",
@@ -405,6 +432,8 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2",
+                    help="BASELINE config; cfg2 is the headline workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full-mode", action="store_true",
                     help="skip timing the reference (full-inverse) formulation")
