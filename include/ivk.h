@@ -226,6 +226,25 @@ int ivk_seed_constrained(int32_t stages, int32_t n_nodes, int32_t n_p,
                          const uint8_t* node_constrained, const double* src,
                          double* out, void* stream);
 
+/* ---- Krylov vector work of FGMRES (solvers.py:388-430), deterministic ----
+ * Reductions use a fixed grid of block partials summed in block order; the
+ * library keeps one small scratch buffer per device. */
+/* *result = <x, y> (device scalar). */
+int ivk_dot(int64_t n, const double* x, const double* y, double* result, void* stream);
+/* *result = ||x||_2 (device scalar). */
+int ivk_norm(int64_t n, const double* x, double* result, void* stream);
+/* Modified Gram-Schmidt of w against V_0..V_{k-1} (rows of V, stride ldv):
+ * h[i] = <w, V_i>; w -= h[i] V_i (i ascending); h[k] = ||w||; if v_next:
+ * v_next = w / h[k] when h[k] > 1e-300 (solvers.py:401-408).  h is device. */
+int ivk_mgs(int64_t n, const double* V, int64_t ldv, int32_t k, double* w, double* h,
+            double* v_next, void* stream);
+/* out = x / coef[k] when coef[k] > 1e-300 (coef device). */
+int ivk_scale(int64_t n, const double* x, const double* coef, int32_t k, double* out,
+              void* stream);
+/* x += sum_i y[i] Z_i, i ascending (solvers.py:432); y device. */
+int ivk_lincomb(int64_t n, const double* Z, int64_t ldz, int32_t k, const double* y, double* x,
+                void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -115,6 +115,11 @@ _SIGS = {
     "ivk_project_pressure_means": ([C.c_int32, C.c_int32, C.c_int32, _P, _P], C.c_int),
     "ivk_axpby": ([C.c_int64, C.c_double, _P, C.c_double, _P, _P, _P], C.c_int),
     "ivk_seed_constrained": ([C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P], C.c_int),
+    "ivk_dot": ([C.c_int64, _P, _P, _P, _P], C.c_int),
+    "ivk_norm": ([C.c_int64, _P, _P, _P], C.c_int),
+    "ivk_mgs": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P, _P], C.c_int),
+    "ivk_scale": ([C.c_int64, _P, _P, C.c_int32, _P, _P], C.c_int),
+    "ivk_lincomb": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P], C.c_int),
 }
 EXPORTED = tuple(_SIGS)
 

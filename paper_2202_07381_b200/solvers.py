@@ -778,31 +778,112 @@ def fgmres(op_apply, b, precond=None, x0=None, rtol=1e-8, atol=0.0, maxiter=100,
 
     Same algorithm as the reference (MGS Arnoldi, Givens rotations, restart,
     true-residual check at each cycle end, monotone reported envelope).
-    Runs on the device when ``b`` is a CUDA tensor (the small Hessenberg
-    least-squares problem stays on the host); numpy ``b`` runs on the host.
+    When ``b`` is a CUDA tensor the Krylov basis lives on the device and the
+    MGS / norms / solution update run in libivk (fused, deterministic
+    reductions); only the (m+1) x m Hessenberg column travels to the host
+    once per iteration for the Givens update.  numpy ``b`` runs on the host.
     """
     if _is_torch(b):
-        import torch
-        dev_ = b.device
-        n = b.numel()
-        x = torch.zeros(n, dtype=torch.float64, device=dev_) if x0 is None else \
-            torch.as_tensor(x0, dtype=torch.float64, device=dev_).clone()
-        norm = lambda v: float(torch.linalg.vector_norm(v))
-        zeros = lambda *s: torch.zeros(*s, dtype=torch.float64, device=dev_)
-        as_vec = lambda v: torch.as_tensor(v, dtype=torch.float64, device=dev_)
-        dot = torch.dot
-    else:
-        n = len(b)
-        x = np.zeros(n) if x0 is None else np.asarray(x0, dtype=float).copy()
-        norm = lambda v: float(np.linalg.norm(v))
-        zeros = lambda *s: np.zeros(s)
-        as_vec = lambda v: np.array(v, dtype=float)
-        dot = lambda u, v: u @ v
+        return _fgmres_device(op_apply, b, precond, x0, rtol, atol, maxiter, restart)
+    n = len(b)
+    x = np.zeros(n) if x0 is None else np.asarray(x0, dtype=float).copy()
     if precond is None:
         precond = lambda v: v
     stats = KrylovStats()
 
     r = b - op_apply(x)
+    norm0 = float(np.linalg.norm(r))
+    stats.residual_norms.append(norm0)
+    tol = max(rtol * norm0, atol)
+    if norm0 <= tol:
+        stats.final_residual = norm0
+        stats.relative_residual = 0.0 if norm0 == 0 else 1.0
+        stats.converged = True
+        return x, stats
+
+    while stats.iterations < maxiter:
+        m = min(restart, maxiter - stats.iterations)
+        V = np.zeros((m + 1, n))
+        Z = np.zeros((m, n))
+        H = np.zeros((m + 1, m))
+        cs = np.zeros(m)
+        sn = np.zeros(m)
+        g = np.zeros(m + 1)
+        beta = np.linalg.norm(r)
+        V[0] = r / beta
+        g[0] = beta
+        k = 0
+        for j in range(m):
+            Z[j] = precond(V[j])
+            w = np.array(op_apply(Z[j]), dtype=float)
+            for i in range(j + 1):
+                H[i, j] = w @ V[i]
+                w -= H[i, j] * V[i]
+            H[j + 1, j] = np.linalg.norm(w)
+            if H[j + 1, j] > 1e-300:
+                V[j + 1] = w / H[j + 1, j]
+            k = _givens_step(H, cs, sn, g, j)
+            stats.iterations += 1
+            est = abs(g[j + 1])
+            stats.residual_norms.append(est)
+            if est <= tol or stats.iterations >= maxiter:
+                break
+        y = np.linalg.solve(np.triu(H[:k, :k]), g[:k])
+        x = x + y @ Z[:k]
+        r = b - op_apply(x)
+        true_norm = float(np.linalg.norm(r))
+        stats.residual_norms[-1] = true_norm
+        if true_norm <= tol:
+            break
+
+    stats.final_residual = float(np.linalg.norm(b - op_apply(x)))
+    stats.relative_residual = stats.final_residual / norm0 if norm0 > 0 else 0.0
+    stats.converged = stats.final_residual <= tol
+    stats.residual_norms = list(np.minimum.accumulate(stats.residual_norms))
+    return x, stats
+
+
+def _givens_step(H, cs, sn, g, j):
+    """Apply the stored rotations to column j and form the new one
+    (solvers.py:409-421); returns j + 1."""
+    for i in range(j):
+        t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+        H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+        H[i, j] = t
+    denom = np.hypot(H[j, j], H[j + 1, j])
+    cs[j] = H[j, j] / denom
+    sn[j] = H[j + 1, j] / denom
+    H[j, j] = denom
+    H[j + 1, j] = 0.0
+    g[j + 1] = -sn[j] * g[j]
+    g[j] = cs[j] * g[j]
+    return j + 1
+
+
+def _fgmres_device(op_apply, b, precond, x0, rtol, atol, maxiter, restart):
+    import torch
+    from ._device import ptr, stream
+    L = _lib.lib()
+    dev_ = b.device
+    n = b.numel()
+    f64 = dict(dtype=torch.float64, device=dev_)
+    x = torch.zeros(n, **f64) if x0 is None else torch.as_tensor(x0, **f64).clone()
+    if precond is None:
+        precond = lambda v: v
+    stats = KrylovStats()
+    scal = torch.zeros(1, **f64)
+
+    def norm(v):
+        _lib.check(L.ivk_norm(n, ptr(v), ptr(scal), stream()), "norm")
+        return float(scal.item())
+
+    def residual(xv):
+        out = torch.empty(n, **f64)
+        _lib.check(L.ivk_axpby(n, 1.0, ptr(b), -1.0, ptr(op_apply(xv)), ptr(out), stream()),
+                   "residual")
+        return out
+
+    r = residual(x)
     norm0 = norm(r)
     stats.residual_norms.append(norm0)
     tol = max(rtol * norm0, atol)
@@ -814,63 +895,39 @@ def fgmres(op_apply, b, precond=None, x0=None, rtol=1e-8, atol=0.0, maxiter=100,
 
     while stats.iterations < maxiter:
         m = min(restart, maxiter - stats.iterations)
-        V = zeros(m + 1, n)
-        Z = zeros(m, n)
+        V = torch.zeros(m + 1, n, **f64)
+        Z = torch.zeros(m, n, **f64)
+        hdev = torch.zeros(m + 2, **f64)
         H = np.zeros((m + 1, m))
         cs = np.zeros(m)
         sn = np.zeros(m)
         g = np.zeros(m + 1)
-
         beta = norm(r)
-        V[0] = r / beta
+        _lib.check(L.ivk_axpby(n, 1.0 / beta, ptr(r), 0.0, None, ptr(V[0]), stream()), "scale")
         g[0] = beta
         k = 0
         for j in range(m):
-            Z[j] = precond(V[j])
-            w = as_vec(op_apply(Z[j]))
-            if _is_torch(w):
-                w = w.clone()
-                hc = zeros(j + 1)
-                for i in range(j + 1):
-                    hc[i] = dot(w, V[i])
-                    w -= hc[i] * V[i]
-                H[:j + 1, j] = hc.cpu().numpy()
-            else:
-                for i in range(j + 1):
-                    H[i, j] = w @ V[i]
-                    w -= H[i, j] * V[i]
-            H[j + 1, j] = norm(w)
-            if H[j + 1, j] > 1e-300:
-                V[j + 1] = w / H[j + 1, j]
-            for i in range(j):
-                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
-                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
-                H[i, j] = t
-            denom = np.hypot(H[j, j], H[j + 1, j])
-            cs[j] = H[j, j] / denom
-            sn[j] = H[j + 1, j] / denom
-            H[j, j] = denom
-            H[j + 1, j] = 0.0
-            g[j + 1] = -sn[j] * g[j]
-            g[j] = cs[j] * g[j]
-            k = j + 1
+            Z[j].copy_(precond(V[j]))
+            w = torch.as_tensor(op_apply(Z[j]), **f64).clone()
+            _lib.check(L.ivk_mgs(n, ptr(V), n, j + 1, ptr(w), ptr(hdev), ptr(V[j + 1]), stream()),
+                       "mgs")
+            H[:j + 2, j] = hdev[:j + 2].cpu().numpy()
+            k = _givens_step(H, cs, sn, g, j)
             stats.iterations += 1
             est = abs(g[j + 1])
             stats.residual_norms.append(est)
             if est <= tol or stats.iterations >= maxiter:
                 break
         y = np.linalg.solve(np.triu(H[:k, :k]), g[:k])
-        if _is_torch(x):
-            x = x + as_vec(y) @ Z[:k]
-        else:
-            x = x + y @ Z[:k]
-        r = b - op_apply(x)
+        ydev = torch.as_tensor(y, **f64)
+        _lib.check(L.ivk_lincomb(n, ptr(Z), n, k, ptr(ydev), ptr(x), stream()), "lincomb")
+        r = residual(x)
         true_norm = norm(r)
         stats.residual_norms[-1] = true_norm
         if true_norm <= tol:
             break
 
-    stats.final_residual = norm(b - op_apply(x))
+    stats.final_residual = norm(residual(x))
     stats.relative_residual = stats.final_residual / norm0 if norm0 > 0 else 0.0
     stats.converged = stats.final_residual <= tol
     stats.residual_norms = list(np.minimum.accumulate(stats.residual_norms))
