@@ -37,6 +37,7 @@ extern "C" {
 #define IVK_EUNSUPPORTED (-4)
 
 #define IVK_MAX_STAGES 3
+#define IVK_MAX_QUAD 16
 
 /* Stage-coupled operator  I_s (x) diag(M, 0) + dt A (x) [[K, B], [B^T, 0]]
  * (+ dt a_ij J_i on the velocity block), with identity rows on constrained
@@ -225,6 +226,38 @@ int ivk_axpby(int64_t n, double alpha, const double* x, double beta, const doubl
 int ivk_seed_constrained(int32_t stages, int32_t n_nodes, int32_t n_p,
                          const uint8_t* node_constrained, const double* src,
                          double* out, void* stream);
+
+/* ---- Convection linearisation at Newton cadence (fem.py:199-242) ----------
+ * Reference-triangle quadrature (points in the collapsed degree-5 rule) with
+ * the P2 basis values and reference gradients at each point. */
+typedef struct ivk_quad_table {
+  int32_t nq;
+  double w[IVK_MAX_QUAD];
+  double phi[IVK_MAX_QUAD * 6];       /* [q][a]                             */
+  double dphi[IVK_MAX_QUAD * 6 * 2];  /* [q][a][e]                          */
+} ivk_quad_table;
+
+typedef struct ivk_convection_desc {
+  int32_t n_cells, n_nodes, nnz;
+  const ivk_quad_table* quad;  /* HOST pointer                            */
+  const int32_t* cell_nodes;   /* C x 6 scalar P2 nodes                    */
+  const double* cell_geo;      /* C x 5: Jinv (row-major [e][d]), det J    */
+  const int32_t* entry_ptr;    /* nnz + 1                                  */
+  const int32_t* entry_contrib;/* cell*36 + a*6 + b, cell-ascending        */
+  const int32_t* row_of;       /* nnz: row node of each pattern entry      */
+  const int32_t* col;          /* nnz: column node                         */
+  const uint8_t* node_constrained; /* eliminated rows/columns -> 0         */
+  const int32_t* sell_pos;     /* nnz: position in the SELL-16 copy        */
+  const int32_t* node_ptr;     /* n_nodes + 1 (residual map)               */
+  const int32_t* node_contrib; /* cell*6 + a                               */
+} ivk_convection_desc;
+
+/* Convection Jacobian J_N(u) of the velocity u (interleaved, 2*n_nodes) on
+ * the scalar P2 pattern, eliminated, written as (Jxx,Jxy,Jyx,Jyy) per entry
+ * to conv (CSR order) and/or conv_s (SELL order); if residual != NULL also
+ * N(u) (interleaved).  elem_scratch: C*144 (+ C*12 with residual) doubles. */
+int ivk_convection_assemble(const ivk_convection_desc* d, const double* u, double* elem_scratch,
+                            double* conv, double* conv_s, double* residual, void* stream);
 
 /* ---- Krylov vector work of FGMRES (solvers.py:388-430), deterministic ----
  * Reductions use a fixed grid of block partials summed in block order; the

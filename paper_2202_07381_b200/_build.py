@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libivk.so")
 SOURCES = ["ivk_operator.cu", "ivk_patches.cu", "ivk_transfer.cu", "ivk_coarse.cu",
-           "ivk_krylov.cu"]
+           "ivk_krylov.cu", "ivk_assembly.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

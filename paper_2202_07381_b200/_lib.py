@@ -11,6 +11,7 @@ __all__ = ["lib", "check", "OperatorDesc", "PatchDesc", "KronDesc", "TransferDes
            "IVK_MAX_STAGES", "IvkError", "SingularPatch"]
 
 IVK_MAX_STAGES = 3
+IVK_MAX_QUAD = 16
 IVK_ESINGULAR = -3
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -96,6 +97,26 @@ class CoarseDesc(C.Structure):
     ]
 
 
+class QuadTable(C.Structure):
+    _fields_ = [
+        ("nq", C.c_int32),
+        ("w", C.c_double * IVK_MAX_QUAD),
+        ("phi", C.c_double * (IVK_MAX_QUAD * 6)),
+        ("dphi", C.c_double * (IVK_MAX_QUAD * 12)),
+    ]
+
+
+class ConvectionDesc(C.Structure):
+    _fields_ = [
+        ("n_cells", C.c_int32), ("n_nodes", C.c_int32), ("nnz", C.c_int32),
+        ("quad", C.POINTER(QuadTable)),
+        ("cell_nodes", C.c_void_p), ("cell_geo", C.c_void_p),
+        ("entry_ptr", C.c_void_p), ("entry_contrib", C.c_void_p),
+        ("row_of", C.c_void_p), ("col", C.c_void_p), ("node_constrained", C.c_void_p),
+        ("sell_pos", C.c_void_p), ("node_ptr", C.c_void_p), ("node_contrib", C.c_void_p),
+    ]
+
+
 # name -> argtypes (restype int unless noted)
 _P = C.c_void_p
 _SIGS = {
@@ -115,6 +136,7 @@ _SIGS = {
     "ivk_project_pressure_means": ([C.c_int32, C.c_int32, C.c_int32, _P, _P], C.c_int),
     "ivk_axpby": ([C.c_int64, C.c_double, _P, C.c_double, _P, _P, _P], C.c_int),
     "ivk_seed_constrained": ([C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P], C.c_int),
+    "ivk_convection_assemble": ([C.POINTER(ConvectionDesc), _P, _P, _P, _P, _P, _P], C.c_int),
     "ivk_dot": ([C.c_int64, _P, _P, _P, _P], C.c_int),
     "ivk_norm": ([C.c_int64, _P, _P, _P], C.c_int),
     "ivk_mgs": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P, _P], C.c_int),

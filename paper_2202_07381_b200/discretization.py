@@ -82,6 +82,15 @@ class Discretization:
         return MGHierarchyOp(levels, coarse, use_graph=use_graph), levels[-1].system
 
 
+    def convection_assemblers(self):
+        """One device ConvectionAssembler per level (MGHierarchyOp.relinearize)."""
+        from .assembly import ConvectionAssembler
+        if not hasattr(self, "_assemblers"):
+            self._assemblers = [ConvectionAssembler(m, b, cm) for m, b, cm in
+                                zip(self.hier.levels, self.blocks, self.cnodes)]
+        return self._assemblers
+
+
 def streamfunction_velocity(points):
     """w = (d psi/dy, -d psi/dx) / pi for psi = sin^2(pi x) sin^2(pi y);
     max |w| = 1 (BASELINE config 3 / SURVEY.md §8(d))."""

@@ -34,6 +34,7 @@ __all__ = [
     "p2_node_coords",
     "assemble_blocks",
     "assemble_convection_jacobian",
+    "assemble_convection_residual",
     "prolongation",
     "velocity_boundary_nodes",
     "velocity_boundary_dofs",
@@ -296,6 +297,25 @@ def assemble_convection_jacobian(mesh, blocks, u):
     if not (np.array_equal(rowptr, blocks.rowptr) and np.array_equal(col, blocks.col)):
         raise RuntimeError("convection pattern differs from the scalar P2 pattern")
     return ConvectionBlocks(blocks.n_nodes, rowptr, col, val.reshape(-1, 2, 2))
+
+
+def assemble_convection_residual(mesh, blocks, u):
+    """N(u)_(a,d) = <(u . grad) u_d, phi_a> (reference ``assemble_convection``
+    with need="residual", fem.py:219-227), interleaved like u."""
+    u = np.asarray(u, dtype=np.float64)
+    nodes = p2_cell_nodes(mesh)
+    _, jinv, det = _affine(mesh)
+    pts, w = triangle_rule(DEG_CONVECTION)
+    phi, dphi = p2_basis(pts)
+    g = _physical_gradients(dphi, jinv)
+    uloc = u.reshape(-1, 2)[nodes]
+    uq = np.einsum("cad,aq->cqd", uloc, phi)
+    gradu = np.einsum("cad,caqe->cqde", uloc, g)
+    conv = np.einsum("cqe,cqde->cqd", uq, gradu)
+    nloc = np.einsum("q,aq,cqd->cad", w, phi, conv, optimize=True) * det[:, None, None]
+    out = np.zeros((blocks.n_nodes, 2))
+    np.add.at(out, nodes.reshape(-1), nloc.reshape(-1, 2))
+    return out.reshape(-1)
 
 
 def prolongation(hierarchy, level, kind):

@@ -726,6 +726,25 @@ class MGHierarchyOp:
         sys_.project_pressure_means(z)
         return z
 
+    def relinearize(self, u, assemblers):
+        """Newton-cadence update: assemble J_N(u_l) on the
+        GPU for every level from the device velocity ``u`` (nodal injection
+        u_l = u[:2 n_l], bench.py:178-185), refactorise every level's patches
+        in place (K7) and re-factor the coarsest operator (host SuperLU, as the
+        reference's coarse_direct_solve)."""
+        if len(assemblers) != len(self.levels):
+            raise ValueError("one ConvectionAssembler per level required")
+        for k, (lev, asm) in enumerate(zip(self.levels, assemblers)):
+            n = 2 * lev.system.n_nodes
+            asm.assemble_into_system(lev.system, u[:n])
+            if k > 0:
+                lev.patches.factor()
+        s0 = self.levels[0].system
+        s0.download_convection()
+        self.coarse = CoarseSolver(s0)
+        self._graph = None
+        self._bufs = None
+
     def _graph_precondition(self, r):
         import torch
         if self._graph is None:

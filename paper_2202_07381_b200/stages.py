@@ -299,6 +299,29 @@ class StageSystem:
                      "cmask_dofs": torch.from_numpy(self._cmask).to(t["cmask"].device)}
         return self._dev
 
+    def sell_pos(self):
+        """Position of every CSR pattern entry in the SELL-16 copy."""
+        b = self.blocks
+        lens = np.diff(b.rowptr)
+        C_ = 16
+        nsl = (self.n_nodes + C_ - 1) // C_
+        padded = np.zeros(nsl * C_, dtype=np.int64)
+        padded[:self.n_nodes] = lens
+        width = padded.reshape(nsl, C_).max(axis=1)
+        sptr = np.concatenate([[0], np.cumsum(width * C_)])
+        rows = np.repeat(np.arange(self.n_nodes), lens)
+        ent = np.arange(len(rows)) - b.rowptr[rows]
+        return sptr[rows // C_] + ent * C_ + rows % C_
+
+    def download_convection(self):
+        """Refresh the host copy of the (single, shared) device convection."""
+        if self._dev is None or "conv" not in self._dev["tensors"]:
+            return
+        v = self._dev["tensors"]["conv"].reshape(-1, 2, 2).cpu().numpy()
+        self._conv_vals = [v]
+        J = ConvectionBlocks(self.n_nodes, self.blocks.rowptr, self.blocks.col, v)
+        self.convection = [J] * self.r
+
     @property
     def desc(self):
         return self.device_data()["desc"]

@@ -252,7 +252,8 @@ def assembly_golden():
         m = disc.hier.levels[1]
         blk = disc.blocks[1]
         u = np.random.default_rng(5).standard_normal(blk.n_u)
-        _, J = rfem.assemble_convection(m, disc.vel[1], u, need="jacobian")
+        N, J = rfem.assemble_convection(m, disc.vel[1], u, need="both")
+        out[f"{grid}_N"] = N
         for name, A in (("M", blk.M), ("K", blk.K), ("B", blk.B), ("J", J),
                         ("P2", rfem.prolongation(disc.hier, 0, "p2")),
                         ("P1", rfem.prolongation(disc.hier, 0, "p1"))):

@@ -43,6 +43,8 @@ STRUCTS = {
     "ivk_kron_desc": _lib.KronDesc,
     "ivk_transfer_desc": _lib.TransferDesc,
     "ivk_coarse_desc": _lib.CoarseDesc,
+    "ivk_quad_table": _lib.QuadTable,
+    "ivk_convection_desc": _lib.ConvectionDesc,
 }
 
 

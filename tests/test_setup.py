@@ -177,3 +177,13 @@ def test_blocks_from_reference_vector_matrices(asm, grid):
     J = sp.csr_matrix(asm[f"{grid}_J"])
     Jb = fem.ConvectionBlocks.from_vector(J, blk)
     assert abs(Jb.matrix - J).max() == 0
+
+
+@pytest.mark.parametrize("grid", ["diagonal", "crossed"])
+def test_convection_residual_matches_reference(asm, grid):
+    h = build_hierarchy(2, 1, grid)
+    m = h.levels[1]
+    blk = fem.assemble_blocks(m, mu=0.7)
+    N = fem.assemble_convection_residual(m, blk, asm[f"{grid}_u"])
+    ref = asm[f"{grid}_N"]
+    assert np.max(np.abs(N - ref)) <= 1e-14 * np.max(np.abs(ref))
