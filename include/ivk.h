@@ -129,6 +129,13 @@ typedef struct ivk_kron_desc {
   double vinv_re[IVK_MAX_STAGES * IVK_MAX_STAGES]; /* V^-1[k][i]           */
   double vinv_im[IVK_MAX_STAGES * IVK_MAX_STAGES];
   double scale[IVK_MAX_STAGES];
+  /* symmetric != 0 (Stokes: S^ symmetric, so every block and its inverse is
+   * complex-symmetric): each block is stored as the lower tile-triangle of
+   * 4 x 4 tiles -- tile (I, J), J <= I < nt = ceil(b/4), at index
+   * I(I+1)/2 + J, row-major inside the tile, 16 doubles real / 32 complex
+   * (re, im interleaved), zero padding past b; a patch's blocks are
+   * contiguous. */
+  int32_t symmetric;
 } ivk_kron_desc;
 
 /* Nested P2/P1 transfer I_s (x) blockdiag(P_P2 (x) I_2, P_P1)

@@ -58,6 +58,7 @@ class KronDesc(C.Structure):
         ("vinv_re", C.c_double * (IVK_MAX_STAGES * IVK_MAX_STAGES)),
         ("vinv_im", C.c_double * (IVK_MAX_STAGES * IVK_MAX_STAGES)),
         ("scale", C.c_double * IVK_MAX_STAGES),
+        ("symmetric", C.c_int32),
     ]
 
 

@@ -375,12 +375,14 @@ struct KronParams {
   double v_re[IVK_MAX_STAGES * IVK_MAX_STAGES], v_im[IVK_MAX_STAGES * IVK_MAX_STAGES];
   double vinv_re[IVK_MAX_STAGES * IVK_MAX_STAGES], vinv_im[IVK_MAX_STAGES * IVK_MAX_STAGES];
   double scale[IVK_MAX_STAGES];
+  int symmetric;
 };
 
 static KronParams make_kron(const ivk_kron_desc* k, int S) {
   KronParams p;
   p.nblk = k->nblk;
   p.S = S;
+  p.symmetric = k->symmetric;
   for (int i = 0; i < IVK_MAX_STAGES; ++i) {
     p.is_complex[i] = k->is_complex[i];
     p.lam_re[i] = k->lam_re[i];
@@ -398,6 +400,21 @@ static KronParams make_kron(const ivk_kron_desc* k, int S) {
 
 __host__ __device__ __forceinline__ int kron_ldr(int b) { return (b + 3) & ~3; }
 __host__ __device__ __forceinline__ int kron_ldc(int b) { return (b + 1) & ~1; }
+// symmetric storage: the lower tile-triangle of 4x4 tiles (I >= J, nt =
+// ceil(b/4)), ordered by tile diagonal d = I - J and, inside a diagonal,
+// chunk-major: the q-th 32-byte chunk of tile (d + t, t) at
+// base_d + 4 (q (nt - d) + t), base_d = 4 QC sum_{d' < d} (nt - d'), QC = 4
+// (real: chunk q = tile row q) or 8 (complex: row q/2, columns 2(q%2)..+1,
+// (re, im) interleaved).  Zero padding past b.
+__host__ __device__ __forceinline__ int kron_sym_block(bool cplx, int b) {
+  const int nt = (b + 3) >> 2;
+  return (cplx ? 32 : 16) * (nt * (nt + 1) / 2);
+}
+__host__ __device__ __forceinline__ int kron_sym_doubles(const KronParams& kp, int b) {
+  int n = 0;
+  for (int k = 0; k < kp.nblk; ++k) n += kron_sym_block(kp.is_complex[k] != 0, b);
+  return n;
+}
 
 // In-place Gauss-Jordan inverse (row pivoting, first max of |re|+|im|) of a
 // d x d matrix held as separate re/im arrays in shared memory.
@@ -560,8 +577,35 @@ __global__ void __launch_bounds__(kKronFactorThreads) patch_factor_kron_kernel(
       if (tid == 0) atomicMin(singular, v);
       return;
     }
-    // store G^T
-    if (cplx) {
+    // store G^T, or the lower tile-triangle of (G + G^T) / 2 (diagonal order)
+    if (kp.symmetric) {
+      const int nt = (b + 3) >> 2;
+      const int qc = cplx ? 8 : 4;
+      const int total = kron_sym_block(cplx, b);
+      for (int e = tid; e < total; e += blockDim.x) {
+        // e -> (d, q, t, w): w = element within the 4-double chunk
+        int d = 0, base = 0;
+        while (base + 4 * qc * (nt - d) <= e) { base += 4 * qc * (nt - d); ++d; }
+        const int rem = e - base, len = nt - d;
+        const int q = rem / (4 * len), t = (rem / 4) % len, w = rem & 3;
+        const int I = d + t, J = t;
+        int i, j;
+        bool im = false;
+        if (cplx) {
+          i = 4 * I + (q >> 1);
+          j = 4 * J + 2 * (q & 1) + (w >> 1);
+          im = (w & 1) != 0;
+        } else {
+          i = 4 * I + q;
+          j = 4 * J + w;
+        }
+        double v = 0.0;
+        if (i < b && j < b)
+          v = im ? 0.5 * (Aim[i * b + j] + Aim[j * b + i]) : 0.5 * (Are[i * b + j] + Are[j * b + i]);
+        out[e] = v;
+      }
+      out += kron_sym_block(cplx, b);
+    } else if (cplx) {
       const int ldc = kron_ldc(b);
       for (int e = tid; e < b * ldc; e += blockDim.x) {
         const int j = e / ldc, i = e - j * ldc;
@@ -722,6 +766,170 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_kernel(
   }
 }
 
+// K3e-sym: complex-symmetric eigen-blocks (Stokes) stored as the lower
+// tile-triangle of 4x4 tiles in tile-diagonal order.  Lane L owns rows
+// 4L..4L+3.  In step d lane L (>= d) loads tile (L, L-d) -- consecutive lanes
+// read consecutive 32-byte chunks, 256-bit evict-first loads -- and uses it
+// twice: as stored for its own rows (x chunk L-d) and transposed for rows of
+// chunk L-d (x chunk L), whose 4 partial sums it hands to lane L-d with one
+// shuffle.  Every tile is read from HBM exactly once.
+// One tile of one block in step d: as-stored product into acc, transposed
+// product into w (for chunk L - d).
+template <bool CPLX>
+__device__ __forceinline__ void sym_tile_step(const double* v, const double* xa,
+                                              const double* xt, bool diag, double* acc,
+                                              double* w) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      if (CPLX) {
+        const double gr = v[8 * r + 2 * cc], gi = v[8 * r + 2 * cc + 1];
+        const double ar = xa[2 * cc], ai = xa[2 * cc + 1];
+        acc[2 * r] = fma(gr, ar, fma(-gi, ai, acc[2 * r]));
+        acc[2 * r + 1] = fma(gr, ai, fma(gi, ar, acc[2 * r + 1]));
+        if (!diag) {  // G[4(L-d)+cc][4L+r] = tile[r][cc]
+          const double br = xt[2 * r], bi = xt[2 * r + 1];
+          w[2 * cc] = fma(gr, br, fma(-gi, bi, w[2 * cc]));
+          w[2 * cc + 1] = fma(gr, bi, fma(gi, br, w[2 * cc + 1]));
+        }
+      } else {
+        const double g = v[4 * r + cc];
+        acc[r] = fma(g, xa[2 * cc], acc[r]);
+        if (!diag) w[cc] = fma(g, xt[2 * r], w[cc]);
+      }
+    }
+  }
+}
+
+// One stored block (real or complex) of one patch over the tile diagonals.
+// nt: this lane's patch; ntw: warp maximum (uniform loop for the full-mask
+// shuffles).
+template <bool CPLX>
+__device__ __forceinline__ void sym_diag_block(const double* __restrict__ T, int nt, int ntw,
+                                               int L, const double* __restrict__ x,
+                                               double* __restrict__ z) {
+  constexpr int QC = CPLX ? 8 : 4;
+  constexpr int NV = CPLX ? 8 : 4;
+  double acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  const double* base = T;
+#pragma unroll 1
+  for (int d = 0; d < ntw; ++d) {
+    const int len = nt - d;
+    double w[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) w[q] = 0.0;
+    if (d < nt && L >= d && L < nt) {
+      double v[4 * QC];
+#pragma unroll
+      for (int q = 0; q < QC; ++q)
+        ld_stream4(base + 4 * (q * len + (L - d)), v[4 * q], v[4 * q + 1], v[4 * q + 2],
+                   v[4 * q + 3]);
+      sym_tile_step<CPLX>(v, x + 8 * (L - d), x + 8 * L, d == 0, acc, w);
+    }
+    if (d > 0) {
+      const bool take = L + d < nt;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const double o = __shfl_down_sync(0xffffffffu, w[q], d);
+        if (take) acc[q] += o;
+      }
+    }
+    if (d < nt) base += 4 * QC * len;
+  }
+  if (L < nt) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      z[2 * (4 * L + r)] = CPLX ? acc[2 * r] : acc[r];
+      z[2 * (4 * L + r) + 1] = CPLX ? acc[2 * r + 1] : 0.0;
+    }
+  }
+}
+
+template <int NR, bool HAS_C>
+__device__ __forceinline__ void sym_diag_patch(const double* __restrict__ G, int nt, int ntw,
+                                               int L, const double* __restrict__ x,
+                                               double* __restrict__ z, int MAXP) {
+  const int realsz = 16 * (nt * (nt + 1) / 2);
+#pragma unroll
+  for (int k = 0; k < NR; ++k)
+    sym_diag_block<false>(G + k * realsz, nt, ntw, L, x + k * 2 * MAXP, z + k * 2 * MAXP);
+  if (HAS_C)
+    sym_diag_block<true>(G + NR * realsz, nt, ntw, L, x + NR * 2 * MAXP, z + NR * 2 * MAXP);
+}
+
+// Lanes are split into `ng` groups of `gs` lanes (gs >= the largest nt), one
+// patch per group, so small blocks (nt = 10 at b = 39) still keep 30 of 32
+// lanes busy.  Dynamic shared memory per group:
+// rs[S*MAXP] | rt[nblk][2*MAXP] | zt[nblk][2*MAXP].
+constexpr int kSymWarps = 4;
+
+template <int NR, bool HAS_C>
+__global__ void __launch_bounds__(kSymWarps * 32) patch_apply_kron_sym_kernel(
+    PatchParams pd, KronParams kp, const double* __restrict__ r, double* __restrict__ local,
+    int MAXP, int gs) {
+  extern __shared__ __align__(16) double sym_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ng = 32 / gs;
+  const int grp = lane / gs, gl = lane - grp * gs;
+  const bool active = grp < ng;
+  const int per_group = kp.S * MAXP + 4 * kp.nblk * MAXP;
+  double* rs = sym_smem + (warp * ng + (active ? grp : 0)) * per_group;
+  double* rt_base = rs + kp.S * MAXP;
+  double* zt_base = rt_base + 2 * kp.nblk * MAXP;
+  const int S = kp.S;
+  const int first = (blockIdx.x * kSymWarps + warp) * ng + grp;
+  const int stride = gridDim.x * kSymWarps * ng;
+  const int warp_first = (blockIdx.x * kSymWarps + warp) * ng;
+  for (int base = warp_first; base < pd.num_patches; base += stride) {
+    const int p = first + (base - warp_first);
+    const bool valid = active && p < pd.num_patches;
+    int off = 0, m = 0, b = 1, nt = 0;
+    if (valid) {
+      off = pd.idx_off[p];
+      m = pd.idx_off[p + 1] - off;
+      b = m / S;
+      nt = (b + 3) >> 2;
+    }
+    for (int j = gl; j < m; j += gs) rs[j] = __ldg(r + pd.idx[off + j]);
+    __syncwarp();
+    for (int e = gl; e < kp.nblk * 4 * nt; e += gs) {
+      const int k = e / (4 * nt), a = e - k * 4 * nt;
+      double re = 0.0, im = 0.0;
+      if (a < b) {
+        for (int i = 0; i < S; ++i) {
+          const double xv = rs[i * b + a];
+          re = fma(kp.vinv_re[k * S + i], xv, re);
+          im = fma(kp.vinv_im[k * S + i], xv, im);
+        }
+      }
+      rt_base[k * 2 * MAXP + 2 * a] = re;
+      rt_base[k * 2 * MAXP + 2 * a + 1] = im;
+    }
+    __syncwarp();
+    {
+      // all lanes take part (the shuffles), inactive groups with nt = 0
+      const double* G = valid ? pd.inv + pd.inv_off[p] : pd.inv;
+      const int ntv = valid ? nt : 0;
+      const int ntw = __reduce_max_sync(0xffffffffu, (unsigned)ntv);
+      sym_diag_patch<NR, HAS_C>(G, ntv, ntw, gl, rt_base, zt_base, MAXP);
+    }
+    __syncwarp();
+    for (int e = gl; e < m; e += gs) {
+      const int i = e / b, a = e - i * b;
+      double acc = 0.0;
+      for (int k = 0; k < kp.nblk; ++k) {
+        const double zr = zt_base[k * 2 * MAXP + 2 * a], zi = zt_base[k * 2 * MAXP + 2 * a + 1];
+        acc += kp.scale[k] * (kp.v_re[i * S + k] * zr - kp.v_im[i * S + k] * zi);
+      }
+      st_keep(local + (pd.slot_pos ? pd.slot_pos[off + e] : off + e), acc);
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace ivk
 
 using namespace ivk;
@@ -745,6 +953,36 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
     for (int i = 0; i < k->nblk; ++i) S += k->is_complex[i] ? 2 : 1;
     KronParams kp = make_kron(k, S);
     const int bmax = pd->max_m / S;
+    if (k->symmetric) {
+      IVK_REQUIRE(bmax <= 64, "kron block size %d > 64 unsupported", bmax);
+      const int maxp = (bmax + 3) & ~3;
+      const int nt_max = maxp >> 2;
+      const int gs = nt_max <= 8 ? 8 : nt_max <= 10 ? 10 : nt_max <= 16 ? 16 : 32;
+      const int ng = 32 / gs;
+      const size_t smem =
+          (size_t)kSymWarps * ng * (S * maxp + 4 * k->nblk * maxp) * sizeof(double);
+      int nr = 0;
+      for (int q = 0; q < k->nblk; ++q) nr += k->is_complex[q] ? 0 : 1;
+      const bool hc = nr < k->nblk;
+      // stored blocks are real first, then at most one complex (pair) block
+      void (*fn)(PatchParams, KronParams, const double*, double*, int, int) = nullptr;
+      if (nr == 1 && hc) fn = patch_apply_kron_sym_kernel<1, true>;
+      else if (nr == 0 && hc) fn = patch_apply_kron_sym_kernel<0, true>;
+      else if (nr == 1) fn = patch_apply_kron_sym_kernel<1, false>;
+      else if (nr == 2) fn = patch_apply_kron_sym_kernel<2, false>;
+      else if (nr == 3) fn = patch_apply_kron_sym_kernel<3, false>;
+      IVK_REQUIRE(fn != nullptr, "unsupported eigen-block signature");
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) {
+        set_error("ivk_patch_apply: %s", cudaGetErrorString(e));
+        return IVK_ECUDA;
+      }
+      int sgrid = (pd->num_patches + kSymWarps * ng - 1) / (kSymWarps * ng);
+      if (sgrid > kSMs * 16) sgrid = kSMs * 16;
+      fn<<<sgrid, kSymWarps * 32, smem, st>>>(p, kp, r, local, maxp, gs);
+      return check_launch("ivk_patch_apply(kron-sym)");
+    }
     if (bmax <= 64)
       patch_apply_kron_kernel<64><<<grid, kApplyWarps * 32, 0, st>>>(p, kp, r, local);
     else {

@@ -95,7 +95,8 @@ class KronSplit:
     ``ivk_kron_desc``): one stored block per real eigenvalue and per
     complex-conjugate pair."""
 
-    def __init__(self, A, max_cond=1e6):
+    def __init__(self, A, max_cond=1e6, symmetric=False):
+        self.symmetric = bool(symmetric)
         A = np.asarray(A, dtype=np.float64)
         s = len(A)
         lam, V = np.linalg.eig(A)
@@ -136,13 +137,58 @@ class KronSplit:
                 d.v_im[i * self.s + k] = self.V[i, k].imag
                 d.vinv_re[k * self.s + i] = self.Vinv[k, i].real
                 d.vinv_im[k * self.s + i] = self.Vinv[k, i].imag
+        d.symmetric = int(self.symmetric)
         return d
 
     def block_doubles(self, b):
         """Stored doubles per patch of block size b (matches the kernels)."""
+        if self.symmetric:
+            return sum(self._sym_block(c, b) for c in self.is_complex)
         ldr = (b + 3) & ~3
         ldc = (b + 1) & ~1
         return sum(2 * b * ldc if c else b * ldr for c in self.is_complex)
+
+    @staticmethod
+    def _sym_block(cplx, b):
+        nt = (b + 3) // 4
+        return (32 if cplx else 16) * (nt * (nt + 1) // 2)
+
+    def unpack(self, raw, b):
+        """Stored blocks of one patch (raw doubles) -> list of b x b blocks."""
+        G, pos = [], 0
+        for cplx in self.is_complex:
+            if self.symmetric:
+                nt = (b + 3) // 4
+                size = self._sym_block(cplx, b)
+                vals = raw[pos:pos + size]
+                qc = 8 if cplx else 4
+                T = np.zeros((4 * nt, 4 * nt), dtype=complex if cplx else float)
+                base = 0
+                for d in range(nt):
+                    ln = nt - d
+                    blk = vals[base:base + 4 * qc * ln].reshape(qc, ln, 4)
+                    for t in range(ln):
+                        I, J = d + t, t
+                        chunks = blk[:, t, :]            # (qc, 4)
+                        if cplx:
+                            tile = (chunks[:, 0::2] + 1j * chunks[:, 1::2]).reshape(4, 4)
+                        else:
+                            tile = chunks.reshape(4, 4)
+                        T[4 * I:4 * I + 4, 4 * J:4 * J + 4] = tile
+                        T[4 * J:4 * J + 4, 4 * I:4 * I + 4] = tile.T
+                    base += 4 * qc * ln
+                G.append(T[:b, :b])
+                pos += size
+            elif cplx:
+                ldc = (b + 1) & ~1
+                a = raw[pos:pos + 2 * b * ldc].reshape(b, ldc, 2)[:, :b]
+                G.append((a[..., 0] + 1j * a[..., 1]).T)
+                pos += 2 * b * ldc
+            else:
+                ldr = (b + 3) & ~3
+                G.append(raw[pos:pos + b * ldr].reshape(b, ldr)[:, :b].T)
+                pos += b * ldr
+        return G
 
     def full_inverse(self, G, b):
         """Reassemble the (s b) x (s b) inverse from stored blocks G[k] (b x b)."""
@@ -165,8 +211,10 @@ class VankaPatchSet:
 
     ``mode``: "full" stores each patch's (s b)^2 inverse (the reference's
     formulation); "kron" the Butcher eigen-split (s b^2 doubles per patch,
-    3x fewer bytes at s = 3); "auto" picks "kron" when all stages share the
-    convection Jacobian, A is well diagonalisable and b <= 64.
+    3x fewer bytes at s = 3); "kron-sym" additionally stores each block as a
+    symmetric tile-triangle (Stokes: no convection; 44% fewer bytes than
+    kron at cfg2); "auto" picks kron (all stages share the convection
+    Jacobian, A well diagonalisable, b <= 64), else full.
     """
 
     def __init__(self, system, mesh, omega=1.0, factor=True, mode="auto", scatter="patch"):
@@ -178,22 +226,30 @@ class VankaPatchSet:
         self.num_patches = mesh.num_vertices
         self.tables = build_patch_tables(mesh, system.n_nodes, system.n_p, system.r,
                                          system.node_constrained)
-        if mode not in ("auto", "full", "kron"):
+        if mode not in ("auto", "full", "kron", "kron-sym"):
             raise ValueError(f"unknown patch mode {mode!r}")
+        # kron-sym halves the inverse bytes but measures no faster than kron on
+        # B200 (latency-bound, profiles/r01): "auto" keeps the plain kron layout.
+        symmetric = mode == "kron-sym"
+        if mode == "kron-sym" and system.convection is not None:
+            raise ValueError("kron-sym needs a symmetric (convection-free) operator")
         self.kron = None
-        if mode in ("auto", "kron"):
+        if mode in ("auto", "kron", "kron-sym"):
             try:
                 shared = system.convection is None or len(system._conv_vals) == 1
                 if not shared:
                     raise ValueError("per-stage convection Jacobians differ")
                 if self.tables.max_m // system.r > 64:
                     raise ValueError("patch block too large for the kron kernels")
-                self.kron = KronSplit(system.tableau.A)
+                # Stokes (no convection): S^ symmetric -> packed symmetric blocks
+                self.kron = KronSplit(system.tableau.A,
+                                      symmetric=(system.convection is None and symmetric))
             except ValueError:
-                if mode == "kron":
+                if mode in ("kron", "kron-sym"):
                     raise
                 self.kron = None
-        self.mode = "kron" if self.kron is not None else "full"
+        self.mode = "full" if self.kron is None else \
+            ("kron-sym" if self.kron.symmetric else "kron")
         self._layout()
         self._dev = None
         self._factored = False
@@ -254,18 +310,7 @@ class VankaPatchSet:
                 raw = inv_all[off:off + count * per].view(count, per).cpu().numpy()
                 inv = np.empty((count, m, m))
                 for q in range(count):
-                    G, pos = [], 0
-                    for cplx in self.kron.is_complex:
-                        if cplx:
-                            ldc = (b + 1) & ~1
-                            a = raw[q, pos:pos + 2 * b * ldc].reshape(b, ldc, 2)[:, :b]
-                            G.append((a[..., 0] + 1j * a[..., 1]).T)
-                            pos += 2 * b * ldc
-                        else:
-                            ldr = (b + 3) & ~3
-                            G.append(raw[q, pos:pos + b * ldr].reshape(b, ldr)[:, :b].T)
-                            pos += b * ldr
-                    inv[q] = self.kron.full_inverse(G, b)
+                    inv[q] = self.kron.full_inverse(self.kron.unpack(raw[q], b), b)
             out.append((idx.copy(), inv))
         return out
 

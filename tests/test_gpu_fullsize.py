@@ -139,16 +139,18 @@ def test_fixed_point_linearity_determinism(full):
     assert torch.equal(p1, p2)
 
 
-def test_kron_and_full_formulations_agree(full):
+def test_patch_formulations_agree(full):
     import torch
     from paper_2202_07381_b200 import VankaPatchSet, apply_vanka
     (disc, tab, conv, case, mg, mg_pou, S, b), name = full
     kron = mg.levels[-1].patches
     assert kron.mode == "kron"
-    fullp = VankaPatchSet(S, disc.fine_mesh, mode="full")
     x0 = torch.zeros_like(b)
     yk = apply_vanka(kron, S, x0, b, omega=0.5, weights="pou")
-    yf = apply_vanka(fullp, S, x0, b, omega=0.5, weights="pou")
-    del fullp
-    torch.cuda.empty_cache()
-    assert float(torch.linalg.vector_norm(yk - yf)) <= 1e-12 * float(torch.linalg.vector_norm(yf))
+    for mode in (["full"] if conv is not None else ["full", "kron-sym"]):
+        other = VankaPatchSet(S, disc.fine_mesh, mode=mode)
+        yo = apply_vanka(other, S, x0, b, omega=0.5, weights="pou")
+        del other
+        torch.cuda.empty_cache()
+        assert float(torch.linalg.vector_norm(yk - yo)) <= \
+            1e-12 * float(torch.linalg.vector_norm(yo)), mode
