@@ -673,7 +673,9 @@ class MGHierarchyOp:
 
     # -- smoothing (fused device versions of solvers.py:321-332) --------------
 
-    def _smooth(self, level, x, b, sweeps):
+    def _smooth(self, level, x, b, sweeps, x_zero=False):
+        """x_zero: x is known to be 0, so the first residual b - A x is b
+        itself (bitwise: A 0 = +0) and its K1 launch is skipped."""
         if sweeps == 0:
             return
         lev = self.levels[level]
@@ -682,9 +684,12 @@ class MGHierarchyOp:
         buf = self._bufs[level]
         w = pat.weights(sm.weighting)
         if sm.accel == "richardson":
-            for _ in range(sweeps):
-                sys_.apply_into(x, b, buf.r)
-                loc = pat.apply_local(buf.r)
+            for k in range(sweeps):
+                if k == 0 and x_zero:
+                    loc = pat.apply_local(b)
+                else:
+                    sys_.apply_into(x, b, buf.r)
+                    loc = pat.apply_local(buf.r)
                 pat.combine(loc, x, 1.0, sm.omega, w, x)
             return
         if sm.accel == "chebyshev":
@@ -693,11 +698,15 @@ class MGHierarchyOp:
             delta = 0.5 * (bb - a)
             sigma1 = theta / delta
             rho = 1.0 / sigma1
-            sys_.apply_into(x, b, buf.r)
-            loc = pat.apply_local(buf.r)
+            if x_zero:
+                loc = pat.apply_local(b)        # r = b
+            else:
+                sys_.apply_into(x, b, buf.r)
+                loc = pat.apply_local(buf.r)
             pat.combine(loc, None, 0.0, sm.omega / theta, w, buf.d, accum=x)
-            for _ in range(1, sweeps):
-                sys_.apply_into(buf.d, buf.r, buf.r)
+            for k in range(1, sweeps):
+                # r = r - A d (with r = b when the first residual was skipped)
+                sys_.apply_into(buf.d, b if (k == 1 and x_zero) else buf.r, buf.r)
                 loc = pat.apply_local(buf.r)
                 rho_new = 1.0 / (2.0 * sigma1 - rho)
                 pat.combine(loc, buf.d, rho_new * rho, 2.0 * rho_new / delta * sm.omega, w,
@@ -717,7 +726,7 @@ class MGHierarchyOp:
                        maxiter=sweeps, restart=sweeps)
         x.copy_(xs)
 
-    def _cycle(self, level, x, b):
+    def _cycle(self, level, x, b, x_zero=False):
         """In place: x <- V-cycle(level, x, b) (solvers.py:334-347)."""
         tr = self.trace
         if level == 0:
@@ -732,7 +741,7 @@ class MGHierarchyOp:
         lev = self.levels[level]
         buf = self._bufs[level]
         below = self._bufs[level - 1]
-        self._smooth(level, x, b, lev.smoother.pre)
+        self._smooth(level, x, b, lev.smoother.pre, x_zero=x_zero)
         if tr is not None:
             tr[f"pre_{level}"] = x.clone()
         lev.system.apply_into(x, b, buf.r)
@@ -740,7 +749,7 @@ class MGHierarchyOp:
         if tr is not None:
             tr[f"rc_{level}"] = below.b.clone()
         below.x.zero_()
-        self._cycle(level - 1, below.x, below.b)
+        self._cycle(level - 1, below.x, below.b, x_zero=True)
         lev.prolong.prolong_add(below.x, x)
         self._smooth(level, x, b, lev.smoother.post)
         if tr is not None:
@@ -807,6 +816,19 @@ class MGHierarchyOp:
         self._g_in.copy_(r)
         self._graph.replay()
         return self._g_out.clone()
+
+    def precondition_to(self, r, out):
+        """Device: out = precondition(r) without allocating (graph or eager)."""
+        self._buffers()
+        if self.use_graph and all(l.smoother.accel != "gmres" for l in self.levels[1:]):
+            if self._graph is None:
+                self._graph_precondition(r)
+            self._g_in.copy_(r)
+            self._graph.replay()
+            out.copy_(self._g_out)
+        else:
+            self.precondition_into(r, out)
+        return out
 
     def precondition(self, r):
         """Preconditioner application for FGMRES: approximately solve A z = r."""
@@ -947,6 +969,16 @@ def _fgmres_device(op_apply, b, precond, x0, rtol, atol, maxiter, restart):
                    "residual")
         return out
 
+    # Allocation-free fast paths for this package's own operator / cycle.
+    pre_to = None
+    if getattr(precond, "__func__", None) is MGHierarchyOp.precondition:
+        pre_to = precond.__self__.precondition_to
+    op_into = None
+    if getattr(getattr(op_apply, "__self__", None), "apply_into", None) is not None and \
+            getattr(op_apply, "__name__", "") == "matvec":
+        sysobj = op_apply.__self__
+        op_into = lambda v, out: sysobj.apply_into(v, None, out)
+
     r = residual(x)
     norm0 = norm(r)
     stats.residual_norms.append(norm0)
@@ -957,6 +989,7 @@ def _fgmres_device(op_apply, b, precond, x0, rtol, atol, maxiter, restart):
         stats.converged = True
         return x, stats
 
+    w = torch.empty(n, **f64)
     while stats.iterations < maxiter:
         m = min(restart, maxiter - stats.iterations)
         V = torch.zeros(m + 1, n, **f64)
@@ -971,8 +1004,14 @@ def _fgmres_device(op_apply, b, precond, x0, rtol, atol, maxiter, restart):
         g[0] = beta
         k = 0
         for j in range(m):
-            Z[j].copy_(precond(V[j]))
-            w = torch.as_tensor(op_apply(Z[j]), **f64).clone()
+            if pre_to is not None:
+                pre_to(V[j], Z[j])
+            else:
+                Z[j].copy_(precond(V[j]))
+            if op_into is not None:
+                op_into(Z[j], w)
+            else:
+                w.copy_(torch.as_tensor(op_apply(Z[j]), **f64))
             _lib.check(L.ivk_mgs(n, ptr(V), n, j + 1, ptr(w), ptr(hdev), ptr(V[j + 1]), stream()),
                        "mgs")
             H[:j + 2, j] = hdev[:j + 2].cpu().numpy()

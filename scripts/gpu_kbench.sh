@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python scripts/kernel_bench.py 50 cfg2 > gpurun_out/kbench.log 2>&1; echo "exit $?" >> gpurun_out/kbench.log
-ncu --set full --clock-control none --import-source on -k regex:"kron_sym" -s 3 -c 1 -o gpurun_out/prof_sym python scripts/kernel_bench.py 5 cfg2 > gpurun_out/ncu_sym.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_krylov.py tests/test_gpu_assembly.py -x -q > gpurun_out/pytest_k.log 2>&1; echo "exit $?" >> gpurun_out/pytest_k.log
+timeout 900 python bench.py --no-cpu-baseline --no-full-mode > gpurun_out/bench.log 2>&1; echo "exit $?" >> gpurun_out/bench.log
