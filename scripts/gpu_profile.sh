@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
 python scripts/prof_workload.py cfg2 > gpurun_out/prof_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg2.csv python scripts/prof_workload.py cfg2 > gpurun_out/ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"patch_apply|stage_apply|patch_combine" -s 0 -c 3 -o gpurun_out/prof_cfg2 python scripts/prof_workload.py cfg2 > gpurun_out/ncu_full.log 2>&1
 echo done

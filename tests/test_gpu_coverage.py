@@ -1,0 +1,104 @@
+"""Breadth of the device path against the CPU oracle (GPU): every Butcher
+tableau family of the reference registry (tableaux.py:114-123) including a
+non-diagonalisable DIRK (falls back to the full formulation), GMRES-
+accelerated smoothing (solvers.py:321-332), partial hierarchies
+(bench.py:212-216) and singular-patch detection (solvers.py:176-183)."""
+
+import numpy as np
+import pytest
+
+from harness import oracle_levels, rel
+from oracle.irk_vanka_oracle import OracleMG, oracle_apply_vanka, random_rhs
+
+pytestmark = pytest.mark.gpu
+
+TABLEAUX = [("gauss", 1), ("gauss", 2), ("gauss", 3), ("radauiia", 1), ("radauiia", 2),
+            ("radauiia", 3), ("lobattoiiic", 2), ("lobattoiiic", 3), ("backwardeuler", 1),
+            ("dirk-pareschirusso", 2)]
+
+
+def _disc(grid="diagonal", n0=4, level=1, mu=1.0):
+    from paper_2202_07381_b200 import Discretization
+    return Discretization(n0, level, mu=mu, grid=grid)
+
+
+@pytest.mark.parametrize("family,stages", TABLEAUX)
+def test_sweep_and_vcycle_every_tableau(family, stages):
+    from paper_2202_07381_b200 import SmootherSpec, apply_vanka, tableau_lookup
+    disc = _disc()
+    tab = tableau_lookup(family, stages)
+    dt = 1.0 / 16
+    sm = SmootherSpec()
+    mg, S = disc.build_mg(tab, dt, sm)
+    fine = mg.levels[-1].patches
+    if family == "dirk-pareschirusso":
+        assert fine.mode == "full"      # repeated eigenvalue: no eigen-split
+    lv = oracle_levels(disc, tab, dt, None)
+    op, pat = lv[-1]["op"], lv[-1]["patches"]
+    b = random_rhs(op, 3)
+    x0 = np.random.default_rng(4).uniform(-1, 1, op.dim)
+    x0[op.constrained_stage_dofs()] = 0.0
+    got = apply_vanka(fine, S, x0, b, omega=0.5)
+    assert rel(got, oracle_apply_vanka(pat, op, x0, b, 0.5)) <= 1e-12
+    omg = OracleMG(lv, dict(pre=2, post=2, accel="chebyshev", a=2.0, b=8.0, omega=1.0,
+                            weights=None))
+    assert rel(mg.precondition(b), omg.precondition(b.copy())) <= 1e-11
+
+
+def test_gmres_accelerated_smoothing_matches_oracle():
+    from paper_2202_07381_b200 import SmootherSpec, fgmres, tableau_lookup
+    disc = _disc(grid="crossed", n0=2, level=1)
+    tab = tableau_lookup("radauiia", 2)
+    sm = SmootherSpec(accel="gmres")
+    mg, S = disc.build_mg(tab, 0.1, sm)
+    lv = oracle_levels(disc, tab, 0.1, None)
+    omg = OracleMG(lv, dict(pre=2, post=2, accel="gmres", omega=1.0, weights=None))
+    b = random_rhs(lv[-1]["op"], 12)
+    assert rel(mg.precondition(b), omg.precondition(b.copy())) <= 1e-10
+    # reference test_gmres_accelerated_smoothing (test_solvers.py:321-334)
+    xs = np.random.default_rng(12).standard_normal(S.dim)
+    xs[S.constrained_stage_dofs()] = 0.0
+    xs = S.project_pressure_means(xs)
+    _, st = fgmres(S.matvec, S.matvec(xs), precond=mg.precondition, rtol=1e-8, maxiter=60,
+                   restart=30)
+    assert st.converged and st.iterations <= 30
+
+
+def test_partial_hierarchy():
+    from paper_2202_07381_b200 import ConfigError, SmootherSpec, tableau_lookup
+    disc = _disc(n0=4, level=2)
+    tab = tableau_lookup("radauiia", 2)
+    mg, S = disc.build_mg(tab, 1 / 16, SmootherSpec(), mg_levels=2)
+    assert len(mg.levels) == 2 and mg.levels[0].system.dim == disc.blocks[1].n_u * 0 + \
+        tab.r * (disc.blocks[1].n_u + disc.blocks[1].n_p)
+    lv = oracle_levels(disc, tab, 1 / 16, None, levels=[1, 2])
+    lv[0]["prolong"] = None
+    omg = OracleMG(lv, dict(pre=2, post=2, accel="chebyshev", a=2.0, b=8.0, omega=1.0,
+                            weights=None))
+    b = random_rhs(lv[-1]["op"], 5)
+    assert rel(mg.precondition(b), omg.precondition(b.copy())) <= 1e-11
+    with pytest.raises(ConfigError):
+        disc.build_mg(tab, 1 / 16, SmootherSpec(), mg_levels=7)
+
+
+def test_singular_patch_detected():
+    from paper_2202_07381_b200 import PatchSingularError, VankaPatchSet, tableau_lookup
+    from paper_2202_07381_b200.stages import StageSystem
+    disc = _disc(n0=2, level=0)
+    tab = tableau_lookup("backwardeuler", 1)
+    # dt = 0: the patch pressure rows vanish -> every patch matrix is singular
+    S = StageSystem(disc.blocks[0], tab, 0.0, disc.cdofs[0])
+    for mode in ("full", "kron"):
+        with pytest.raises(PatchSingularError) as ei:
+            VankaPatchSet(S, disc.hier.levels[0], mode=mode)
+        assert 0 <= ei.value.vertex < disc.hier.levels[0].num_vertices
+
+
+def test_invalid_arguments_raise():
+    from paper_2202_07381_b200 import SmootherSpec, apply_vanka, tableau_lookup
+    disc = _disc(n0=2, level=1)
+    mg, S = disc.build_mg(tableau_lookup("radauiia", 2), 0.1, SmootherSpec())
+    with pytest.raises(ValueError):
+        S.matvec(np.zeros(S.dim + 1))
+    with pytest.raises(ValueError):
+        apply_vanka(mg.levels[-1].patches, S, np.zeros(3), np.zeros(S.dim))
