@@ -8,7 +8,9 @@
 //
 // Tile-sparse blocked substitution: the factors are stored as 32 x 32 tiles
 // (column-major), only the ~1/3 nonzero ones.  Per block column K one warp
-// solves the diagonal tile with register shuffles, its tiles streamed two
+// solves the diagonal tile -- L's (unit, well-conditioned) diagonal tiles are
+// stored inverted and applied as a GEMV, U's by a register-shuffle
+// substitution with stored reciprocal diagonal -- its tiles streamed two
 // steps ahead into a shared-memory ring by TMA bulk copies (cp.async.bulk +
 // mbarrier); the other 15 warps hold the (already prefetched) off-diagonal
 // tiles of column K in registers and apply the rank-32 update as soon as y_K
@@ -109,12 +111,19 @@ __device__ void tile_solve(int nb, const int32_t* colptr, const int32_t* rowtile
       const double* D = ring + slot * 1024;
       double yl = y[K * 32 + lane];
       if (LOWER) {
+        // the lower diagonal tiles are stored inverted (tile_factor): a
+        // 32 x 32 GEMV instead of a 32-step shuffle chain
+        const double* yk = y + K * 32;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
-          const double d = D[jj * 32 + lane];
-          const double yj = __shfl_sync(0xffffffffu, yl, jj);
-          if (lane > jj) yl = fma(-d, yj, yl);
+        for (int jj = 0; jj < 32; jj += 4) {
+          a0 = fma(D[jj * 32 + lane], yk[jj], a0);
+          a1 = fma(D[(jj + 1) * 32 + lane], yk[jj + 1], a1);
+          a2 = fma(D[(jj + 2) * 32 + lane], yk[jj + 2], a2);
+          a3 = fma(D[(jj + 3) * 32 + lane], yk[jj + 3], a3);
         }
+        __syncwarp();
+        yl = (a0 + a1) + (a2 + a3);
       } else {
         // the diagonal slot of an upper tile holds 1 / U_jj (tile_factor)
 #pragma unroll

@@ -21,6 +21,7 @@ from dataclasses import dataclass, field
 from typing import Optional
 
 import numpy as np
+import scipy.linalg as sla
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
@@ -526,7 +527,8 @@ class CoarseSolver:
 
     def tiles(self):
         """Tile-sparse (32 x 32, column-major tiles) copies of the factors."""
-        return tile_factor(self.lu.L, lower=True), tile_factor(self.lu.U, lower=False)
+        return (tile_factor(self.lu.L, lower=True, invert_lower_diag=True),
+                tile_factor(self.lu.U, lower=False))
 
     def device_data(self):
         if self._dev is not None:
@@ -567,7 +569,7 @@ class CoarseSolver:
         return to_host(x) if host else x
 
 
-def tile_factor(F, lower, tile=32):
+def tile_factor(F, lower, tile=32, invert_lower_diag=False):
     """Split a triangular factor into dense tile x tile blocks (column-major
     inside a tile), keeping only nonzero off-diagonal tiles, grouped by
     block column.  Padding rows/columns get a unit diagonal."""
@@ -590,6 +592,12 @@ def tile_factor(F, lower, tile=32):
         k = np.arange(nb)[:, None]
         i = np.arange(tile)[None, :]
         diag[k, i, i] = 1.0 / diag[k, i, i]
+    elif invert_lower_diag:
+        # unit lower 32 x 32 diagonal tiles -> their inverses (the device
+        # applies them as a GEMV; numerics within SuperLU's own floor, F9)
+        eye = np.eye(tile)
+        for k in range(nb):
+            diag[k] = sla.solve_triangular(diag[k], eye, lower=True, unit_diagonal=True)
     off = ~on
     key = bj[off].astype(np.int64) * nb + bi[off]
     ukey, inv = np.unique(key, return_inverse=True)
