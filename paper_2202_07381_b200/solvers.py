@@ -436,6 +436,13 @@ class VankaPatchSet:
     def weights(self, weighting):
         return None if weighting == "none" else self.device_data()["pou"]
 
+    def workspace(self):
+        """Fresh per-stream sweep scratch (see ``apply_vanka``)."""
+        import torch
+        dev = self.device_data()
+        return {"r": torch.empty(self.tables.dim, dtype=torch.float64, device=dev["idx"].device),
+                "local": torch.empty_like(dev["local"])}
+
     def solve_additive(self, resid):
         """z = sum_i R_i^T (R_i A R_i^T)^{-1} R_i resid (solvers.py:214-222)."""
         from ._device import as_device_vector, to_host
@@ -454,11 +461,15 @@ def build_vanka_patches(system, mesh, omega=1.0):
     return VankaPatchSet(system, mesh, omega=omega)
 
 
-def apply_vanka(patches, system, x, b, omega=None, weights=None):
+def apply_vanka(patches, system, x, b, omega=None, weights=None, workspace=None, out=None):
     """One additive Schwarz sweep x + omega W sum R_i^T A_i^-1 R_i (b - A x)
     (solvers.py:232-239) as one fused K1 -> K3 -> K4 pass.
 
-    ``weights``: None (reference, unweighted), "pou", or a DoF vector."""
+    ``weights``: None (reference, unweighted), "pou", or a DoF vector.
+    ``workspace``: optional dict with device scratch "r" (dim) and "local"
+    (total_m) -- one per stream when sweeps run concurrently on several
+    streams (the patch set's own scratch is shared).  ``out``: optional
+    device output buffer."""
     from ._device import as_device_vector, ptr, stream, to_host, upload
     import torch
     w = patches.omega if omega is None else omega
@@ -472,10 +483,14 @@ def apply_vanka(patches, system, x, b, omega=None, weights=None):
         wd, _ = as_device_vector(weights, system.dim)
     patches._require()
     dev = patches.device_data()
-    r = torch.empty_like(xd)
-    out = torch.empty_like(xd)
+    if workspace is not None:
+        r, local = workspace["r"], workspace["local"]
+    else:
+        r, local = torch.empty_like(xd), dev["local"]
+    if out is None:
+        out = torch.empty_like(xd)
     _lib.check(_lib.lib().ivk_vanka_sweep(system.desc, dev["desc"], ptr(xd), ptr(bd), float(w),
-                                          ptr(wd), ptr(r), ptr(dev["local"]), ptr(out), stream()),
+                                          ptr(wd), ptr(r), ptr(local), ptr(out), stream()),
                "vanka_sweep")
     return to_host(out) if host else out
 

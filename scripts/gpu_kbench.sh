@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -k "vcycle or fgmres" > gpurun_out/pytest_k.log 2>&1; echo "exit $?" >> gpurun_out/pytest_k.log
-timeout 600 python scripts/kernel_bench.py 50 cfg2 > gpurun_out/kbench.log 2>&1; echo "exit $?" >> gpurun_out/kbench.log
+timeout 900 python bench.py --no-cpu-baseline --no-full-mode > gpurun_out/bench.log 2>&1; echo "exit $?" >> gpurun_out/bench.log
