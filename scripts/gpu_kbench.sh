@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python bench.py --no-cpu-baseline --no-full-mode > gpurun_out/bench.log 2>&1; echo "exit $?" >> gpurun_out/bench.log
+timeout 900 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_short.log 2>&1; echo "exit $?" >> gpurun_out/bench_short.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "exit $?" >> gpurun_out/bench.log
