@@ -107,6 +107,20 @@ typedef struct ivk_patch_desc {
                               local[dof_ptr[d] .. dof_ptr[d+1]) contiguously);
                               NULL = patch order, scatter gathers via dof_pos */
   const struct ivk_kron_desc* kron; /* HOST pointer; NULL = full inverses */
+  /* Dedup (kron only; class_of == NULL: per-patch inverses).  Patches whose
+   * canonical stage-coupled matrices are bitwise identical share one set of
+   * inverse blocks: patch p gathers r in canonical order, local position
+   * perm[idx_off[p] + i] of its own layout for canonical position i, applies
+   * the blocks at class_inv + class_inv_off[class_of[p]]; patches are
+   * processed in `order` (grouped by class).  ivk_patch_factor on a
+   * descriptor of the class representatives (canonical node lists) fills
+   * class_inv. */
+  int32_t n_classes;
+  const int32_t* class_of;
+  const uint8_t* perm;
+  const int32_t* order;
+  const int64_t* class_inv_off;
+  const double* class_inv;
 } ivk_patch_desc;
 
 /* Kronecker eigen-split of the patch matrices.  With all stages sharing one

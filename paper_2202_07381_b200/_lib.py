@@ -71,6 +71,9 @@ class PatchDesc(C.Structure):
         ("vertex", C.c_void_p), ("node_off", C.c_void_p), ("node", C.c_void_p),
         ("slot_pos", C.c_void_p),
         ("kron", C.POINTER(KronDesc)),
+        ("n_classes", C.c_int32),
+        ("class_of", C.c_void_p), ("perm", C.c_void_p), ("order", C.c_void_p),
+        ("class_inv_off", C.c_void_p), ("class_inv", C.c_void_p),
     ]
 
 

@@ -34,6 +34,17 @@ struct PatchParams {
   const int32_t* __restrict__ slot_pos;
 };
 
+// dedup tables (kept out of PatchParams: the per-patch kernels' register
+// allocation is sensitive to their parameter block)
+struct DedupParams {
+  int n_classes;
+  const int32_t* __restrict__ class_of;
+  const uint8_t* __restrict__ perm;
+  const int32_t* __restrict__ order;
+  const int64_t* __restrict__ class_inv_off;
+  const double* __restrict__ class_inv;
+};
+
 static PatchParams make_patch_params(const ivk_patch_desc* d) {
   PatchParams p;
   p.num_patches = d->num_patches;
@@ -629,6 +640,20 @@ __global__ void __launch_bounds__(kKronFactorThreads) patch_factor_kron_kernel(
 // Warp per patch.  Gather r_p, transform to the eigenbasis, one streamed
 // GEMV per stored block (lanes split into G groups of CPC lanes; each lane
 // owns a 32-byte row chunk, groups take interleaved columns), back-transform.
+// Inverse-block loads: streamed once (evict-first) per patch, or -- dedup --
+// read-only cached: a class's blocks are shared by thousands of patches.
+template <bool CACHED>
+__device__ __forceinline__ void ld_blk4(const double* p, double& a, double& b, double& c,
+                                        double& d) {
+  if (CACHED) {
+    const double2 x = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 y = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    a = x.x; b = x.y; c = y.x; d = y.y;
+  } else {
+    ld_stream4(p, a, b, c, d);
+  }
+}
+
 template <int MAXB>
 __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_kernel(
     PatchParams pd, KronParams kp, const double* __restrict__ r, double* __restrict__ local) {
@@ -761,6 +786,152 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_kernel(
         acc += kp.scale[k] * (kp.v_re[i * S + k] * zr - kp.v_im[i * S + k] * zi);
       }
       st_keep(local + (pd.slot_pos ? pd.slot_pos[off + e] : off + e), acc);
+    }
+    __syncwarp();
+  }
+}
+
+// K3d: the dedup variant of K3e (class blocks shared, canonical gather/scatter);
+// kept as a separate kernel so the per-patch K3e keeps its ptxas schedule.
+template <int MAXB, bool DEDUP>
+__global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_dedup_kernel(
+    PatchParams pd, DedupParams dd, KronParams kp, const double* __restrict__ r,
+    double* __restrict__ local) {
+  constexpr int MAXM = IVK_MAX_STAGES * MAXB;
+  __shared__ __align__(16) double rs_all[kApplyWarps][MAXM];
+  __shared__ __align__(16) double rt_all[kApplyWarps][IVK_MAX_STAGES][2 * MAXB];
+  __shared__ __align__(16) double red_all[kApplyWarps][32 * 4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* rs = rs_all[warp];
+  double* red = red_all[warp];
+  const int S = kp.S;
+  const int stride = gridDim.x * kApplyWarps;
+  for (int q = blockIdx.x * kApplyWarps + warp; q < pd.num_patches; q += stride) {
+    // dedup: patches in class order so a CTA's warps share (L1-resident) blocks
+    const int p = DEDUP ? dd.order[q] : q;
+    const int off = pd.idx_off[p];
+    const int m = pd.idx_off[p + 1] - off;
+    const int b = m / S;
+    // dedup: gather in the class's canonical order
+    for (int j = lane; j < m; j += 32)
+      rs[j] = __ldg(r + pd.idx[off + (DEDUP ? (int)dd.perm[off + j] : j)]);
+    __syncwarp();
+    // r~_k[a] = sum_i Vinv[k][i] r[i][a]
+    for (int e = lane; e < kp.nblk * b; e += 32) {
+      const int k = e / b, a = e - k * b;
+      double re = 0.0, im = 0.0;
+      for (int i = 0; i < S; ++i) {
+        const double x = rs[i * b + a];
+        re = fma(kp.vinv_re[k * S + i], x, re);
+        im = fma(kp.vinv_im[k * S + i], x, im);
+      }
+      rt_all[warp][k][2 * a] = re;
+      rt_all[warp][k][2 * a + 1] = im;
+    }
+    __syncwarp();
+    const double* G = DEDUP ? dd.class_inv + dd.class_inv_off[dd.class_of[p]]
+                            : pd.inv + pd.inv_off[p];
+    for (int k = 0; k < kp.nblk; ++k) {
+      double* rt = rt_all[warp][k];
+      const bool cplx = kp.is_complex[k] != 0;
+      const int ldd = cplx ? 2 * kron_ldc(b) : kron_ldr(b);  // doubles per column
+      const int cpc = ldd >> 2;                               // 32-byte chunks per column
+      const int groups = 32 / cpc;
+      const int g = lane / cpc, c = lane - g * cpc;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (g < groups) {
+        const double* col = G + 4 * c;
+        int j = g;
+        if (cplx) {
+          for (; j + 3 * groups < b; j += 4 * groups) {
+            double v[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              ld_blk4<DEDUP>(col + (long)(j + u * groups) * ldd, v[u][0], v[u][1], v[u][2], v[u][3]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double xr = rt[2 * (j + u * groups)], xi = rt[2 * (j + u * groups) + 1];
+              a0 = fma(v[u][0], xr, fma(-v[u][1], xi, a0));
+              a1 = fma(v[u][0], xi, fma(v[u][1], xr, a1));
+              a2 = fma(v[u][2], xr, fma(-v[u][3], xi, a2));
+              a3 = fma(v[u][2], xi, fma(v[u][3], xr, a3));
+            }
+          }
+          for (; j < b; j += groups) {
+            double v0, v1, v2, v3;
+            ld_blk4<DEDUP>(col + (long)j * ldd, v0, v1, v2, v3);
+            const double xr = rt[2 * j], xi = rt[2 * j + 1];
+            a0 = fma(v0, xr, fma(-v1, xi, a0));
+            a1 = fma(v0, xi, fma(v1, xr, a1));
+            a2 = fma(v2, xr, fma(-v3, xi, a2));
+            a3 = fma(v2, xi, fma(v3, xr, a3));
+          }
+        } else {
+          for (; j + 3 * groups < b; j += 4 * groups) {
+            double v[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              ld_blk4<DEDUP>(col + (long)(j + u * groups) * ldd, v[u][0], v[u][1], v[u][2], v[u][3]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double x = rt[2 * (j + u * groups)];
+              a0 = fma(v[u][0], x, a0);
+              a1 = fma(v[u][1], x, a1);
+              a2 = fma(v[u][2], x, a2);
+              a3 = fma(v[u][3], x, a3);
+            }
+          }
+          for (; j < b; j += groups) {
+            double v0, v1, v2, v3;
+            ld_blk4<DEDUP>(col + (long)j * ldd, v0, v1, v2, v3);
+            const double x = rt[2 * j];
+            a0 = fma(v0, x, a0);
+            a1 = fma(v1, x, a1);
+            a2 = fma(v2, x, a2);
+            a3 = fma(v3, x, a3);
+          }
+        }
+      }
+      red[4 * lane + 0] = a0;
+      red[4 * lane + 1] = a1;
+      red[4 * lane + 2] = a2;
+      red[4 * lane + 3] = a3;
+      __syncwarp();
+      // z~_k[a] = sum over groups; overwrite rt[k] (no longer needed)
+      if (cplx) {
+        for (int a = lane; a < b; a += 32) {
+          const int ch = a >> 1, q = (a & 1) * 2;
+          double re = 0.0, im = 0.0;
+          for (int gg = 0; gg < groups; ++gg) {
+            re += red[4 * (gg * cpc + ch) + q];
+            im += red[4 * (gg * cpc + ch) + q + 1];
+          }
+          rt[2 * a] = re;
+          rt[2 * a + 1] = im;
+        }
+        G += 2L * b * kron_ldc(b);
+      } else {
+        for (int a = lane; a < b; a += 32) {
+          const int ch = a >> 2, q = a & 3;
+          double re = 0.0;
+          for (int gg = 0; gg < groups; ++gg) re += red[4 * (gg * cpc + ch) + q];
+          rt[2 * a] = re;
+          rt[2 * a + 1] = 0.0;
+        }
+        G += (long)b * kron_ldr(b);
+      }
+      __syncwarp();
+    }
+    // z[i][a] = sum_k scale_k Re(V[i][k] z~_k[a])
+    for (int e = lane; e < m; e += 32) {
+      const int i = e / b, a = e - i * b;
+      double acc = 0.0;
+      for (int k = 0; k < kp.nblk; ++k) {
+        const double zr = rt_all[warp][k][2 * a], zi = rt_all[warp][k][2 * a + 1];
+        acc += kp.scale[k] * (kp.v_re[i * S + k] * zr - kp.v_im[i * S + k] * zi);
+      }
+      const int le = DEDUP ? off + (int)dd.perm[off + e] : off + e;
+      st_keep(local + (pd.slot_pos ? pd.slot_pos[le] : le), acc);
     }
     __syncwarp();
   }
@@ -983,7 +1154,19 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       fn<<<sgrid, kSymWarps * 32, smem, st>>>(p, kp, r, local, maxp, gs);
       return check_launch("ivk_patch_apply(kron-sym)");
     }
-    if (bmax <= 64)
+    if (bmax <= 64 && pd->class_of) {
+      IVK_REQUIRE(pd->perm && pd->order && pd->class_inv_off && pd->class_inv,
+                  "dedup descriptor has a NULL array");
+      DedupParams dd;
+      dd.n_classes = pd->n_classes;
+      dd.class_of = pd->class_of;
+      dd.perm = pd->perm;
+      dd.order = pd->order;
+      dd.class_inv_off = pd->class_inv_off;
+      dd.class_inv = pd->class_inv;
+      patch_apply_kron_dedup_kernel<64, true><<<grid, kApplyWarps * 32, 0, st>>>(p, dd, kp, r,
+                                                                                 local);
+    } else if (bmax <= 64)
       patch_apply_kron_kernel<64><<<grid, kApplyWarps * 32, 0, st>>>(p, kp, r, local);
     else {
       set_error("ivk_patch_apply: kron block size %d > 64 unsupported", bmax);

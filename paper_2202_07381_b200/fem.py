@@ -76,14 +76,20 @@ def _physical_gradients(dphi, jinv):
     return np.einsum("aqe,ced->caqd", dphi, jinv)
 
 
-def _coo_to_csr(rows, cols, vals, n_rows, n_cols):
+def _coo_to_csr(rows, cols, vals, n_rows, n_cols, canonical=False):
     """Deterministic COO -> CSR: entries sorted by (row, col), duplicates
-    summed in input order.  ``vals`` may carry trailing value axes."""
+    summed in input order -- or, with ``canonical``, in ascending order of
+    their values, so that equal multisets of contributions give bitwise
+    equal sums wherever they occur (translation-invariant assembly).
+    ``vals`` may carry trailing value axes."""
     rows = rows.reshape(-1).astype(np.int64)
     cols = cols.reshape(-1).astype(np.int64)
     vals = vals.reshape(len(rows), -1)
     key = rows * n_cols + cols
-    order = np.argsort(key, kind="stable")
+    if canonical:
+        order = np.lexsort(tuple(vals[:, k] for k in range(vals.shape[1] - 1, -1, -1)) + (key,))
+    else:
+        order = np.argsort(key, kind="stable")
     key = key[order]
     vals = vals[order]
     first = np.flatnonzero(np.concatenate(([True], key[1:] != key[:-1])))
@@ -228,8 +234,30 @@ class ConvectionBlocks:
         return sp.csr_matrix((self.val.ravel(), (r.ravel(), c.ravel())), shape=(n, n))
 
 
+class _CanonicalCells:
+    """The mesh with every cell's vertices rotated (cyclically, orientation
+    kept) to start at its lowest-then-leftmost vertex, so congruent cells
+    get bitwise-identical element matrices (exact dyadic geometry)."""
+
+    def __init__(self, mesh):
+        p = mesh.vertices[mesh.cells]
+        y, x = p[:, :, 1], p[:, :, 0]
+        s = np.lexsort((x.T, y.T), axis=0)[0]             # lowest y, then lowest x
+        rot = (s[:, None] + np.arange(3)[None, :]) % 3
+        self.cells = np.take_along_axis(mesh.cells, rot, axis=1)
+        self.cell_to_edges = np.take_along_axis(mesh.cell_to_edges, rot, axis=1)
+        self.vertices = mesh.vertices
+        self.num_vertices = mesh.num_vertices
+        self.num_edges = mesh.num_edges
+
+
 def assemble_blocks(mesh, mu=1.0):
-    """Scalar-form M, K (times mu) and B for one mesh level."""
+    """Scalar-form M, K (times mu) and B for one mesh level.
+
+    Translation-invariant: element matrices are computed on canonically
+    rotated cells and duplicates are summed in value order, so patches with
+    the same local geometry get bitwise-identical matrices (patch dedup)."""
+    mesh = _CanonicalCells(mesh)
     nodes = p2_cell_nodes(mesh)
     n_nodes = mesh.num_vertices + mesh.num_edges
     _, jinv, det = _affine(mesh)
@@ -247,7 +275,7 @@ def assemble_blocks(mesh, mu=1.0):
     rows = np.repeat(nodes[:, :, None], 6, axis=2)
     cols = np.repeat(nodes[:, None, :], 6, axis=1)
     rowptr, col, mk = _coo_to_csr(rows, cols, np.stack([mloc, kloc], axis=-1),
-                                  n_nodes, n_nodes)
+                                  n_nodes, n_nodes, canonical=True)
 
     pts, w = triangle_rule(DEG_DIVERGENCE)
     _, dphi = p2_basis(pts)
@@ -257,7 +285,8 @@ def assemble_blocks(mesh, mu=1.0):
     bloc = -np.einsum("q,bq,caqd->cabd", w, psi, g) * det[:, None, None, None]
     brows = np.repeat(nodes[:, :, None], 3, axis=2)
     bcols = np.repeat(mesh.cells[:, None, :], 6, axis=1)
-    b_rowptr, b_col, b_val = _coo_to_csr(brows, bcols, bloc, n_nodes, mesh.num_vertices)
+    b_rowptr, b_col, b_val = _coo_to_csr(brows, bcols, bloc, n_nodes, mesh.num_vertices,
+                                         canonical=True)
 
     return StokesBlocks(n_nodes=n_nodes, n_p=mesh.num_vertices,
                         rowptr=rowptr, col=col,

@@ -214,8 +214,11 @@ class VankaPatchSet:
     formulation); "kron" the Butcher eigen-split (s b^2 doubles per patch,
     3x fewer bytes at s = 3); "kron-sym" additionally stores each block as a
     symmetric tile-triangle (Stokes: no convection; 44% fewer bytes than
-    kron at cfg2); "auto" picks kron (all stages share the convection
-    Jacobian, A well diagonalisable, b <= 64), else full.
+    kron at cfg2); "dedup" shares the kron blocks of patches whose
+    canonical matrices are bitwise identical (translation-invariant
+    operators: dedup.py); "auto" picks dedup when it collapses the patch
+    set at least 8x (convection-free), else kron (all stages share the
+    convection Jacobian, A well diagonalisable, b <= 64), else full.
     """
 
     def __init__(self, system, mesh, omega=1.0, factor=True, mode="auto", scatter="patch"):
@@ -227,7 +230,7 @@ class VankaPatchSet:
         self.num_patches = mesh.num_vertices
         self.tables = build_patch_tables(mesh, system.n_nodes, system.n_p, system.r,
                                          system.node_constrained)
-        if mode not in ("auto", "full", "kron", "kron-sym"):
+        if mode not in ("auto", "full", "kron", "kron-sym", "dedup"):
             raise ValueError(f"unknown patch mode {mode!r}")
         # kron-sym halves the inverse bytes but measures no faster than kron on
         # B200 (latency-bound, profiles/r01): "auto" keeps the plain kron layout.
@@ -235,7 +238,10 @@ class VankaPatchSet:
         if mode == "kron-sym" and system.convection is not None:
             raise ValueError("kron-sym needs a symmetric (convection-free) operator")
         self.kron = None
-        if mode in ("auto", "kron", "kron-sym"):
+        self.dedup = None
+        if mode == "dedup" and system.convection is not None:
+            raise ValueError("dedup needs a translation-invariant (convection-free) operator")
+        if mode in ("auto", "kron", "kron-sym", "dedup"):
             try:
                 shared = system.convection is None or len(system._conv_vals) == 1
                 if not shared:
@@ -246,11 +252,21 @@ class VankaPatchSet:
                 self.kron = KronSplit(system.tableau.A,
                                       symmetric=(system.convection is None and symmetric))
             except ValueError:
-                if mode in ("kron", "kron-sym"):
+                if mode in ("kron", "kron-sym", "dedup"):
                     raise
                 self.kron = None
+        if self.kron is not None and (mode == "dedup" or (mode == "auto" and
+                                                           system.convection is None)):
+            # translation-invariant operator: share inverses between patches
+            # whose canonical matrices are bitwise identical (dedup.py); "auto"
+            # keeps it only when it actually collapses the patch set
+            from .dedup import build_dedup_tables
+            dd = build_dedup_tables(mesh, system, self.tables)
+            if mode == "dedup" or dd.n_classes * 8 <= self.tables.num_patches:
+                self.dedup = dd
         self.mode = "full" if self.kron is None else \
-            ("kron-sym" if self.kron.symmetric else "kron")
+            ("dedup" if self.dedup is not None else
+             ("kron-sym" if self.kron.symmetric else "kron"))
         self._layout()
         self._dev = None
         self._factored = False
@@ -259,6 +275,13 @@ class VankaPatchSet:
 
     def _layout(self):
         t = self.tables
+        if self.dedup is not None:
+            # per-class (representative) inverse blocks only
+            sizes = np.array([self.kron.block_doubles(int(t.sizes[q]) // t.stages)
+                              for q in self.dedup.rep], dtype=np.int64)
+            off = np.concatenate([[0], np.cumsum(sizes)])
+            self.inv_off, self.inv_size = off[:-1], int(off[-1])
+            return
         if self.kron is None:
             self.inv_off, self.inv_size = t.inv_off, t.inv_size
         else:
@@ -298,6 +321,25 @@ class VankaPatchSet:
         dev = self.device_data()
         inv_all = dev["inv"]
         out = []
+        if self.dedup is not None:
+            dd = self.dedup
+            raw = inv_all.cpu().numpy()
+            cls_inv = []
+            for c_, q in enumerate(dd.rep):
+                b = int(t.sizes[q]) // t.stages
+                o = int(self.inv_off[c_])
+                cls_inv.append(self.kron.full_inverse(
+                    self.kron.unpack(raw[o:o + self.kron.block_doubles(b)], b), b))
+            for m, first, count in t.groups():
+                idx = t.idx[t.idx_off[first]:t.idx_off[first + count]].reshape(count, m)
+                inv = np.empty((count, m, m))
+                for qq in range(count):
+                    q = first + qq
+                    pm = dd.perm[t.idx_off[q]:t.idx_off[q + 1]].astype(np.int64)
+                    G = cls_inv[dd.class_of[q]]
+                    inv[qq][np.ix_(pm, pm)] = G
+                out.append((idx.copy(), inv))
+            return out
         for m, first, count in t.groups():
             idx = t.idx[t.idx_off[first]:t.idx_off[first + count]].reshape(count, m)
             off = int(self.inv_off[first])
@@ -364,6 +406,41 @@ class VankaPatchSet:
         if self.kron is not None:
             d["kron"] = self.kron.desc()          # keep the host struct alive
             desc.kron = C.pointer(d["kron"])
+        if self.dedup is not None:
+            dd = self.dedup
+            d["class_of"] = upload(dd.class_of, np.int32)
+            d["perm"] = upload(dd.perm, np.uint8)
+            d["order"] = upload(dd.order, np.int32)
+            desc.n_classes = dd.n_classes
+            desc.class_of = d["class_of"].data_ptr()
+            desc.perm = d["perm"].data_ptr()
+            desc.order = d["order"].data_ptr()
+            desc.class_inv_off = d["inv_off"].data_ptr()
+            desc.class_inv = d["inv"].data_ptr()
+            # the class representatives as a patch set of their own (K7 input)
+            sizes = t.sizes[dd.rep]
+            rep_idx_off = np.concatenate([[0], np.cumsum(sizes)])
+            rep_node_off = np.concatenate([[0], np.cumsum([len(n) for n in dd.rep_nodes])])
+            d["rep_idx_off"] = upload(rep_idx_off, np.int32)
+            d["rep_node_off"] = upload(rep_node_off, np.int32)
+            d["rep_node"] = upload(np.concatenate(dd.rep_nodes), np.int32)
+            d["rep_vertex"] = upload(dd.rep_vertex, np.int32)
+            rd = _lib.PatchDesc()
+            rd.num_patches = dd.n_classes
+            rd.dim = t.dim
+            rd.max_m = int(sizes.max())
+            rd.total_m = int(rep_idx_off[-1])
+            rd.idx_off = d["rep_idx_off"].data_ptr()
+            rd.idx = d["idx"].data_ptr()            # unused by K7
+            rd.inv_off = d["inv_off"].data_ptr()
+            rd.inv = d["inv"].data_ptr()
+            rd.dof_ptr = d["dof_ptr"].data_ptr()    # unused by K7
+            rd.dof_pos = d["dof_pos"].data_ptr()
+            rd.vertex = d["rep_vertex"].data_ptr()
+            rd.node_off = d["rep_node_off"].data_ptr()
+            rd.node = d["rep_node"].data_ptr()
+            rd.kron = C.pointer(d["kron"])
+            d["rep_desc"] = rd
         d["desc"] = desc
         self._dev = d
         return d
@@ -378,7 +455,8 @@ class VankaPatchSet:
         from ._device import ptr, stream
         dev = self.device_data()
         flag = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev["idx"].device)
-        _lib.check(_lib.lib().ivk_patch_factor(self.system.desc, dev["desc"], ptr(flag), stream()),
+        target = dev["rep_desc"] if self.dedup is not None else dev["desc"]
+        _lib.check(_lib.lib().ivk_patch_factor(self.system.desc, target, ptr(flag), stream()),
                    "patch_factor")
         bad = int(flag.item())
         if bad != 2 ** 31 - 1:
@@ -392,6 +470,7 @@ class VankaPatchSet:
         t = self.tables
         if self.kron is not None:       # reference inverses are full (s b)^2 blocks
             self.kron = None
+            self.dedup = None
             self.mode = "full"
             self._layout()
             self._dev = None

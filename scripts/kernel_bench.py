@@ -49,8 +49,10 @@ def main():
     b0 = torch.randn(S0.dim, dtype=torch.float64, device="cuda")
     x0 = torch.empty_like(b0)
     out["coarse_us"] = timeit(lambda: cs.solve_into(b0, x0), reps)
-    for mode in (("kron-sym", "kron", "full") if conv is None else ("kron", "full")):
-        for scatter in ("patch", "owner"):
+    modes = sys.argv[3].split(",") if len(sys.argv) > 3 else \
+        (["kron", "dedup", "kron-sym", "full"] if conv is None else ["kron", "full"])
+    for mode in modes:
+        for scatter in ("patch",):
             pat = VankaPatchSet(S, disc.fine_mesh, mode=mode, scatter=scatter)
             dev = pat.device_data()
             w = pat.weights("pou")

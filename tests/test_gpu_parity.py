@@ -36,7 +36,8 @@ class Case:
         self.mode = mode
         self.mg, self.S = self.disc.build_mg(self.tab, c["dt"], cheb, convection=self.conv,
                                              patch_mode=mode)
-        expect = mode if mode != "auto" else "kron"
+        expect = mode if mode != "auto" else \
+            ("kron" if c["conv"] or name == "crossed" else "dedup")
         assert self.mg.levels[-1].patches.mode == expect
         pou = SmootherSpec(pre=2, post=2, accel="richardson", omega=0.5, weighting="pou")
         self.mg_pou = MGHierarchyOp([MGLevel(l.system, l.patches, pou, l.prolong)
@@ -48,11 +49,11 @@ class Case:
 _cache = {}
 
 
-@pytest.fixture(params=[(n, m) for n in CASES for m in ("auto", "kron-sym", "full")],
+@pytest.fixture(params=[(n, m) for n in CASES for m in ("auto", "kron-sym", "dedup", "full")],
                 ids=lambda p: f"{p[0]}-{p[1]}")
 def case(request):
-    if request.param == ("ns", "kron-sym"):
-        pytest.skip("kron-sym needs a convection-free (symmetric) operator")
+    if request.param in (("ns", "kron-sym"), ("ns", "dedup")):
+        pytest.skip("kron-sym / dedup need a convection-free operator")
     if request.param not in _cache:
         _cache.clear()   # one case resident at a time
         _cache[request.param] = Case(*request.param)
