@@ -107,20 +107,24 @@ typedef struct ivk_patch_desc {
                               local[dof_ptr[d] .. dof_ptr[d+1]) contiguously);
                               NULL = patch order, scatter gathers via dof_pos */
   const struct ivk_kron_desc* kron; /* HOST pointer; NULL = full inverses */
-  /* Dedup (kron only; class_of == NULL: per-patch inverses).  Patches whose
+  /* Dedup (kron only; n_classes == 0: per-patch inverses).  Patches whose
    * canonical stage-coupled matrices are bitwise identical share one set of
-   * inverse blocks: patch p gathers r in canonical order, local position
-   * perm[idx_off[p] + i] of its own layout for canonical position i, applies
-   * the blocks at class_inv + class_inv_off[class_of[p]]; patches are
-   * processed in `order` (grouped by class).  ivk_patch_factor on a
+   * inverse blocks (class_inv + class_inv_off[c]); ivk_patch_factor on a
    * descriptor of the class representatives (canonical node lists) fills
-   * class_inv. */
+   * class_inv.  The apply runs over tiles of <= 32 same-class patches, in
+   * class order: tile t holds tile_start[t+1] - tile_start[t] patches of
+   * class tile_class[t]; its patches' DoFs, each patch in the class's
+   * canonical order, are cidx[tile_off[t] .. tile_off[t+1]) (gather indices
+   * into r) and cdst[...] (write positions in local[]). */
   int32_t n_classes;
-  const int32_t* class_of;
-  const uint8_t* perm;
-  const int32_t* order;
-  const int64_t* class_inv_off;
+  const int64_t* class_inv_off; /* n_classes + 1 */
   const double* class_inv;
+  int32_t n_tiles;
+  const int32_t* tile_start;    /* n_tiles + 1 */
+  const int32_t* tile_class;    /* n_tiles     */
+  const int32_t* tile_off;      /* n_tiles + 1 */
+  const int32_t* cidx;          /* total_m     */
+  const int32_t* cdst;          /* total_m     */
 } ivk_patch_desc;
 
 /* Kronecker eigen-split of the patch matrices.  With all stages sharing one

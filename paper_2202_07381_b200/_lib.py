@@ -72,8 +72,9 @@ class PatchDesc(C.Structure):
         ("slot_pos", C.c_void_p),
         ("kron", C.POINTER(KronDesc)),
         ("n_classes", C.c_int32),
-        ("class_of", C.c_void_p), ("perm", C.c_void_p), ("order", C.c_void_p),
         ("class_inv_off", C.c_void_p), ("class_inv", C.c_void_p),
+        ("n_tiles", C.c_int32), ("tile_start", C.c_void_p), ("tile_class", C.c_void_p),
+        ("tile_off", C.c_void_p), ("cidx", C.c_void_p), ("cdst", C.c_void_p),
     ]
 
 

@@ -37,12 +37,14 @@ struct PatchParams {
 // dedup tables (kept out of PatchParams: the per-patch kernels' register
 // allocation is sensitive to their parameter block)
 struct DedupParams {
-  int n_classes;
-  const int32_t* __restrict__ class_of;
-  const uint8_t* __restrict__ perm;
-  const int32_t* __restrict__ order;
+  int n_classes, n_tiles;
   const int64_t* __restrict__ class_inv_off;
   const double* __restrict__ class_inv;
+  const int32_t* __restrict__ tile_start;
+  const int32_t* __restrict__ tile_class;
+  const int32_t* __restrict__ tile_off;
+  const int32_t* __restrict__ cidx;
+  const int32_t* __restrict__ cdst;
 };
 
 static PatchParams make_patch_params(const ivk_patch_desc* d) {
@@ -640,20 +642,6 @@ __global__ void __launch_bounds__(kKronFactorThreads) patch_factor_kron_kernel(
 // Warp per patch.  Gather r_p, transform to the eigenbasis, one streamed
 // GEMV per stored block (lanes split into G groups of CPC lanes; each lane
 // owns a 32-byte row chunk, groups take interleaved columns), back-transform.
-// Inverse-block loads: streamed once (evict-first) per patch, or -- dedup --
-// read-only cached: a class's blocks are shared by thousands of patches.
-template <bool CACHED>
-__device__ __forceinline__ void ld_blk4(const double* p, double& a, double& b, double& c,
-                                        double& d) {
-  if (CACHED) {
-    const double2 x = __ldg(reinterpret_cast<const double2*>(p));
-    const double2 y = __ldg(reinterpret_cast<const double2*>(p) + 1);
-    a = x.x; b = x.y; c = y.x; d = y.y;
-  } else {
-    ld_stream4(p, a, b, c, d);
-  }
-}
-
 template <int MAXB>
 __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_kernel(
     PatchParams pd, KronParams kp, const double* __restrict__ r, double* __restrict__ local) {
@@ -791,149 +779,215 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_kernel(
   }
 }
 
-// K3d: the dedup variant of K3e (class blocks shared, canonical gather/scatter);
-// kept as a separate kernel so the per-patch K3e keeps its ptxas schedule.
-template <int MAXB, bool DEDUP>
-__global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_dedup_kernel(
+// K3d: dedup -- class-batched eigen-block GEMM.  Patches of one class share
+// their blocks, so a tile of up to kClassTile same-class patches is one small
+// GEMM per block, Z_k = G_k R_k (b x b times b x T), with G_k staged once in
+// shared memory and reused across the tile from registers: each lane owns a
+// 2-row x 2-patch complex (or 4 x 4 real) micro-tile, i.e. 16 FMAs per 8
+// doubles of shared-memory operands.  Per tile: gather r in the class's
+// canonical order (perm) -> V^-1 transform -> GEMM -> V back-transform ->
+// scatter to each patch's own local[] layout.  Tiles cover `order` contiguously
+// (tile_start), grouped by class; a CTA reloads G only when the class changes.
+constexpr int kClassTile = 32;
+constexpr int kClassCtas = 2;   // resident CTAs per SM (smem ~98 KB at cfg2)
+constexpr int kClassWarps = 8;
+
+__device__ __forceinline__ void cgemm_item(const double* __restrict__ G, const double* __restrict__ R,
+                                           double* __restrict__ Z, int b, int ldc, int i0, int t0) {
+  // rows i0, i0+1; patches t0, t0+1; complex, (re, im) interleaved
+  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 2
+  for (int j = 0; j < b; ++j) {
+    const double2 g0 = *reinterpret_cast<const double2*>(G + 2 * (j * ldc + i0));
+    const double2 g1 = *reinterpret_cast<const double2*>(G + 2 * (j * ldc + i0) + 2);
+    const double2 x0 = *reinterpret_cast<const double2*>(R + 2 * (j * kClassTile + t0));
+    const double2 x1 = *reinterpret_cast<const double2*>(R + 2 * (j * kClassTile + t0) + 2);
+    a[0] = fma(g0.x, x0.x, fma(-g0.y, x0.y, a[0]));
+    a[1] = fma(g0.x, x0.y, fma(g0.y, x0.x, a[1]));
+    a[2] = fma(g0.x, x1.x, fma(-g0.y, x1.y, a[2]));
+    a[3] = fma(g0.x, x1.y, fma(g0.y, x1.x, a[3]));
+    a[4] = fma(g1.x, x0.x, fma(-g1.y, x0.y, a[4]));
+    a[5] = fma(g1.x, x0.y, fma(g1.y, x0.x, a[5]));
+    a[6] = fma(g1.x, x1.x, fma(-g1.y, x1.y, a[6]));
+    a[7] = fma(g1.x, x1.y, fma(g1.y, x1.x, a[7]));
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+    if (i0 + r < b)
+      *reinterpret_cast<double4*>(Z + 2 * ((i0 + r) * kClassTile + t0)) =
+          make_double4(a[4 * r], a[4 * r + 1], a[4 * r + 2], a[4 * r + 3]);
+}
+
+__device__ __forceinline__ void rgemm_item(const double* __restrict__ G, const double* __restrict__ R,
+                                           double* __restrict__ Z, int b, int ldr, int i0, int t0) {
+  // rows i0..i0+3; patches t0..t0+3; real
+  double a[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) a[u] = 0.0;
+#pragma unroll 2
+  for (int j = 0; j < b; ++j) {
+    const double4 g = *reinterpret_cast<const double4*>(G + j * ldr + i0);
+    const double4 x = *reinterpret_cast<const double4*>(R + j * kClassTile + t0);
+    const double gv[4] = {g.x, g.y, g.z, g.w};
+    const double xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) a[4 * r + t] = fma(gv[r], xv[t], a[4 * r + t]);
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    if (i0 + r < b)
+      *reinterpret_cast<double4*>(Z + (i0 + r) * kClassTile + t0) =
+          make_double4(a[4 * r], a[4 * r + 1], a[4 * r + 2], a[4 * r + 3]);
+}
+
+// S stages, NR real eigen-blocks first, then (S - NR) / 2 complex pair blocks:
+// the transforms unroll completely, so V / V^-1 / scale are immediate
+// constant-bank operands.
+template <int S, int NR>
+__global__ void __launch_bounds__(kClassWarps * 32, kClassCtas) patch_apply_class_kernel(
     PatchParams pd, DedupParams dd, KronParams kp, const double* __restrict__ r,
-    double* __restrict__ local) {
-  constexpr int MAXM = IVK_MAX_STAGES * MAXB;
-  __shared__ __align__(16) double rs_all[kApplyWarps][MAXM];
-  __shared__ __align__(16) double rt_all[kApplyWarps][IVK_MAX_STAGES][2 * MAXB];
-  __shared__ __align__(16) double red_all[kApplyWarps][32 * 4];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* rs = rs_all[warp];
-  double* red = red_all[warp];
-  const int S = kp.S;
-  const int stride = gridDim.x * kApplyWarps;
-  for (int q = blockIdx.x * kApplyWarps + warp; q < pd.num_patches; q += stride) {
-    // dedup: patches in class order so a CTA's warps share (L1-resident) blocks
-    const int p = DEDUP ? dd.order[q] : q;
-    const int off = pd.idx_off[p];
-    const int m = pd.idx_off[p + 1] - off;
+    double* __restrict__ local, int g_doubles) {
+  constexpr int NB = NR + (S - NR) / 2;
+  constexpr int T = kClassTile;
+  constexpr int GU = 16;  // gather / scatter loads in flight per thread
+  extern __shared__ __align__(32) double csm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mt = pd.max_m * T;     // R / Z region size (doubles)
+  double* Gs = csm;                // class blocks (+ slack)
+  double* Rs = csm + g_doubles;    // transformed residuals, block-major
+  double* Zs = Rs + mt;            // raw gather, then block results
+  int cur_class = -1;
+  for (int tile = blockIdx.x; tile < dd.n_tiles; tile += gridDim.x) {
+    const int cnt = dd.tile_start[tile + 1] - dd.tile_start[tile];
+    const int cls = dd.tile_class[tile];
+    const int toff = dd.tile_off[tile];
+    const int m = (dd.tile_off[tile + 1] - toff) / cnt;
     const int b = m / S;
-    // dedup: gather in the class's canonical order
-    for (int j = lane; j < m; j += 32)
-      rs[j] = __ldg(r + pd.idx[off + (DEDUP ? (int)dd.perm[off + j] : j)]);
-    __syncwarp();
-    // r~_k[a] = sum_i Vinv[k][i] r[i][a]
-    for (int e = lane; e < kp.nblk * b; e += 32) {
-      const int k = e / b, a = e - k * b;
-      double re = 0.0, im = 0.0;
-      for (int i = 0; i < S; ++i) {
-        const double x = rs[i * b + a];
-        re = fma(kp.vinv_re[k * S + i], x, re);
-        im = fma(kp.vinv_im[k * S + i], x, im);
-      }
-      rt_all[warp][k][2 * a] = re;
-      rt_all[warp][k][2 * a + 1] = im;
+    if (cls != cur_class) {
+      // every CTA thread has finished the previous tile (trailing sync)
+      const double* src = dd.class_inv + dd.class_inv_off[cls];
+      const int nd = (int)(dd.class_inv_off[cls + 1] - dd.class_inv_off[cls]);
+      for (int e = tid; e < nd / 2; e += blockDim.x)
+        reinterpret_cast<double2*>(Gs)[e] = __ldg(reinterpret_cast<const double2*>(src) + e);
+      cur_class = cls;
     }
-    __syncwarp();
-    const double* G = DEDUP ? dd.class_inv + dd.class_inv_off[dd.class_of[p]]
-                            : pd.inv + pd.inv_off[p];
-    for (int k = 0; k < kp.nblk; ++k) {
-      double* rt = rt_all[warp][k];
-      const bool cplx = kp.is_complex[k] != 0;
-      const int ldd = cplx ? 2 * kron_ldc(b) : kron_ldr(b);  // doubles per column
-      const int cpc = ldd >> 2;                               // 32-byte chunks per column
-      const int groups = 32 / cpc;
-      const int g = lane / cpc, c = lane - g * cpc;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      if (g < groups) {
-        const double* col = G + 4 * c;
-        int j = g;
-        if (cplx) {
-          for (; j + 3 * groups < b; j += 4 * groups) {
-            double v[4][4];
+    // gather (canonical order; the tile's gather list is contiguous), zero
+    // padding past cnt; all index loads, then all value loads, in flight
+    {
+      const int n = cnt * m, nt = T * m;
+      const int32_t* ci = dd.cidx + toff;
+      for (int e0 = tid; e0 < nt; e0 += GU * blockDim.x) {
+        int ix[GU];
+        double v[GU];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-              ld_blk4<DEDUP>(col + (long)(j + u * groups) * ldd, v[u][0], v[u][1], v[u][2], v[u][3]);
+        for (int u = 0; u < GU; ++u) {
+          const int e = e0 + u * blockDim.x;
+          ix[u] = e < n ? __ldg(ci + e) : -1;
+        }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const double xr = rt[2 * (j + u * groups)], xi = rt[2 * (j + u * groups) + 1];
-              a0 = fma(v[u][0], xr, fma(-v[u][1], xi, a0));
-              a1 = fma(v[u][0], xi, fma(v[u][1], xr, a1));
-              a2 = fma(v[u][2], xr, fma(-v[u][3], xi, a2));
-              a3 = fma(v[u][2], xi, fma(v[u][3], xr, a3));
-            }
-          }
-          for (; j < b; j += groups) {
-            double v0, v1, v2, v3;
-            ld_blk4<DEDUP>(col + (long)j * ldd, v0, v1, v2, v3);
-            const double xr = rt[2 * j], xi = rt[2 * j + 1];
-            a0 = fma(v0, xr, fma(-v1, xi, a0));
-            a1 = fma(v0, xi, fma(v1, xr, a1));
-            a2 = fma(v2, xr, fma(-v3, xi, a2));
-            a3 = fma(v2, xi, fma(v3, xr, a3));
-          }
+        for (int u = 0; u < GU; ++u) v[u] = ix[u] >= 0 ? __ldg(r + ix[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+          const int e = e0 + u * blockDim.x;
+          if (e < nt) Zs[e] = v[u];
+        }
+      }
+    }
+    __syncthreads();
+    // r~_k[a][t] = sum_i Vinv[k][i] r_t[i b + a]; real blocks [b][T], complex [b][T] x 2
+    for (int e = tid; e < b * T; e += blockDim.x) {
+      const int a = e / T, t = e % T;
+      double x[S];
+#pragma unroll
+      for (int i = 0; i < S; ++i) x[i] = Zs[t * m + i * b + a];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+          re = fma(kp.vinv_re[k * S + i], x[i], re);
+          if (k >= NR) im = fma(kp.vinv_im[k * S + i], x[i], im);
+        }
+        if (k < NR)
+          Rs[k * b * T + e] = re;
+        else
+          *reinterpret_cast<double2*>(Rs + (NR + 2 * (k - NR)) * b * T + 2 * e) =
+              make_double2(re, im);
+      }
+    }
+    __syncthreads();
+    // GEMM items: complex blocks as 8-row x 16-patch warp tiles, real blocks as
+    // 512/T-row x T-patch warp tiles (16 FMAs per column either way)
+    {
+      const int ci = ((b + 7) >> 3) * (T / 16);   // items per complex block
+      constexpr int RQ = 128 / T;                 // real: RQ row quads x T/4 patch quads
+      const int ri = (b + 4 * RQ - 1) / (4 * RQ); // items per real block
+      const int n_items = NR * ri + (NB - NR) * ci;
+      for (int it = warp; it < n_items; it += kClassWarps) {
+        if (it < NR * ri) {
+          const int k = it / ri, li = it - k * ri;
+          rgemm_item(Gs + k * b * kron_ldr(b), Rs + k * b * T, Zs + k * b * T, b, kron_ldr(b),
+                     4 * RQ * li + 4 * (lane % RQ), 4 * (lane / RQ));
         } else {
-          for (; j + 3 * groups < b; j += 4 * groups) {
-            double v[4][4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              ld_blk4<DEDUP>(col + (long)(j + u * groups) * ldd, v[u][0], v[u][1], v[u][2], v[u][3]);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const double x = rt[2 * (j + u * groups)];
-              a0 = fma(v[u][0], x, a0);
-              a1 = fma(v[u][1], x, a1);
-              a2 = fma(v[u][2], x, a2);
-              a3 = fma(v[u][3], x, a3);
-            }
-          }
-          for (; j < b; j += groups) {
-            double v0, v1, v2, v3;
-            ld_blk4<DEDUP>(col + (long)j * ldd, v0, v1, v2, v3);
-            const double x = rt[2 * j];
-            a0 = fma(v0, x, a0);
-            a1 = fma(v1, x, a1);
-            a2 = fma(v2, x, a2);
-            a3 = fma(v3, x, a3);
-          }
+          const int kc = (it - NR * ri) / ci, li = it - NR * ri - kc * ci;
+          const int goff = NR * b * kron_ldr(b) + kc * 2 * b * kron_ldc(b);
+          const int roff = (NR + 2 * kc) * b * T;
+          const int rg = li / (T / 16), pg = li - rg * (T / 16);
+          cgemm_item(Gs + goff, Rs + roff, Zs + roff, b, kron_ldc(b), 8 * rg + 2 * (lane & 3),
+                     16 * pg + 2 * (lane >> 2));
         }
       }
-      red[4 * lane + 0] = a0;
-      red[4 * lane + 1] = a1;
-      red[4 * lane + 2] = a2;
-      red[4 * lane + 3] = a3;
-      __syncwarp();
-      // z~_k[a] = sum over groups; overwrite rt[k] (no longer needed)
-      if (cplx) {
-        for (int a = lane; a < b; a += 32) {
-          const int ch = a >> 1, q = (a & 1) * 2;
-          double re = 0.0, im = 0.0;
-          for (int gg = 0; gg < groups; ++gg) {
-            re += red[4 * (gg * cpc + ch) + q];
-            im += red[4 * (gg * cpc + ch) + q + 1];
-          }
-          rt[2 * a] = re;
-          rt[2 * a + 1] = im;
-        }
-        G += 2L * b * kron_ldc(b);
-      } else {
-        for (int a = lane; a < b; a += 32) {
-          const int ch = a >> 2, q = a & 3;
-          double re = 0.0;
-          for (int gg = 0; gg < groups; ++gg) re += red[4 * (gg * cpc + ch) + q];
-          rt[2 * a] = re;
-          rt[2 * a + 1] = 0.0;
-        }
-        G += (long)b * kron_ldr(b);
-      }
-      __syncwarp();
     }
-    // z[i][a] = sum_k scale_k Re(V[i][k] z~_k[a])
-    for (int e = lane; e < m; e += 32) {
-      const int i = e / b, a = e - i * b;
-      double acc = 0.0;
-      for (int k = 0; k < kp.nblk; ++k) {
-        const double zr = rt_all[warp][k][2 * a], zi = rt_all[warp][k][2 * a + 1];
-        acc += kp.scale[k] * (kp.v_re[i * S + k] * zr - kp.v_im[i * S + k] * zi);
+    __syncthreads();
+    // z_t[i b + a] = sum_k scale_k Re(V[i][k] z~_k[a][t]) into Rs as [t][m]
+    for (int e = tid; e < b * T; e += blockDim.x) {
+      const int a = e / T, t = e % T;
+      double zr[NB], zi[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        if (k < NR) {
+          zr[k] = Zs[k * b * T + e];
+          zi[k] = 0.0;
+        } else {
+          const double2 z =
+              *reinterpret_cast<const double2*>(Zs + (NR + 2 * (k - NR)) * b * T + 2 * e);
+          zr[k] = z.x;
+          zi[k] = z.y;
+        }
       }
-      const int le = DEDUP ? off + (int)dd.perm[off + e] : off + e;
-      st_keep(local + (pd.slot_pos ? pd.slot_pos[le] : le), acc);
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          if (k < NR)
+            acc += kp.scale[k] * kp.v_re[i * S + k] * zr[k];
+          else
+            acc += kp.scale[k] * (kp.v_re[i * S + k] * zr[k] - kp.v_im[i * S + k] * zi[k]);
+        }
+        Rs[t * m + i * b + a] = acc;
+      }
     }
-    __syncwarp();
+    __syncthreads();
+    // scatter to each patch's own local[] layout (slot-fastest: near-contiguous)
+    {
+      const int n = cnt * m;
+      const int32_t* cd = dd.cdst + toff;
+      for (int e0 = tid; e0 < n; e0 += GU * blockDim.x) {
+        int ix[GU];
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+          const int e = e0 + u * blockDim.x;
+          ix[u] = e < n ? __ldg(cd + e) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < GU; ++u)
+          if (ix[u] >= 0) st_keep(local + ix[u], Rs[e0 + u * blockDim.x]);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1154,18 +1208,42 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       fn<<<sgrid, kSymWarps * 32, smem, st>>>(p, kp, r, local, maxp, gs);
       return check_launch("ivk_patch_apply(kron-sym)");
     }
-    if (bmax <= 64 && pd->class_of) {
-      IVK_REQUIRE(pd->perm && pd->order && pd->class_inv_off && pd->class_inv,
+    if (bmax <= 64 && pd->n_classes > 0) {
+      IVK_REQUIRE(pd->class_inv_off && pd->class_inv && pd->tile_start && pd->tile_class &&
+                      pd->tile_off && pd->cidx && pd->cdst && pd->n_tiles > 0,
                   "dedup descriptor has a NULL array");
       DedupParams dd;
       dd.n_classes = pd->n_classes;
-      dd.class_of = pd->class_of;
-      dd.perm = pd->perm;
-      dd.order = pd->order;
+      dd.n_tiles = pd->n_tiles;
       dd.class_inv_off = pd->class_inv_off;
       dd.class_inv = pd->class_inv;
-      patch_apply_kron_dedup_kernel<64, true><<<grid, kApplyWarps * 32, 0, st>>>(p, dd, kp, r,
-                                                                                 local);
+      dd.tile_start = pd->tile_start;
+      dd.tile_class = pd->tile_class;
+      dd.tile_off = pd->tile_off;
+      dd.cidx = pd->cidx;
+      dd.cdst = pd->cdst;
+      int g = 0;
+      for (int q = 0; q < k->nblk; ++q)
+        g += k->is_complex[q] ? 2 * bmax * kron_ldc(bmax) : bmax * kron_ldr(bmax);
+      g = ((g + 3) & ~3) + 32;  // slack: edge micro-tiles read past the last column
+      const size_t smem = (size_t)(g + 2 * pd->max_m * kClassTile) * sizeof(double);
+      int nr = 0;
+      for (int q = 0; q < k->nblk; ++q) nr += k->is_complex[q] ? 0 : 1;
+      void (*fn)(PatchParams, DedupParams, KronParams, const double*, double*, int) = nullptr;
+      if (S == 1 && nr == 1) fn = patch_apply_class_kernel<1, 1>;
+      else if (S == 2 && nr == 2) fn = patch_apply_class_kernel<2, 2>;
+      else if (S == 2 && nr == 0) fn = patch_apply_class_kernel<2, 0>;
+      else if (S == 3 && nr == 3) fn = patch_apply_class_kernel<3, 3>;
+      else if (S == 3 && nr == 1) fn = patch_apply_class_kernel<3, 1>;
+      IVK_REQUIRE(fn != nullptr, "unsupported eigen-block signature");
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) {
+        set_error("ivk_patch_apply: %s", cudaGetErrorString(e));
+        return IVK_ECUDA;
+      }
+      int cgrid = pd->n_tiles < kClassCtas * kSMs ? pd->n_tiles : kClassCtas * kSMs;
+      fn<<<cgrid, kClassWarps * 32, smem, st>>>(p, dd, kp, r, local, g);
     } else if (bmax <= 64)
       patch_apply_kron_kernel<64><<<grid, kApplyWarps * 32, 0, st>>>(p, kp, r, local);
     else {

@@ -31,6 +31,11 @@ class DedupTables:
     rep: np.ndarray           # (n_classes,) flat slot of each class representative
     rep_nodes: list           # canonical free-node list of each representative
     rep_vertex: np.ndarray    # (n_classes,) centre vertex of each representative
+    tile_start: np.ndarray    # (n_tiles + 1,) tiles of <= CLASS_TILE same-class patches
+    tile_class: np.ndarray    # (n_tiles,)    over `order`
+
+
+CLASS_TILE = 32               # kClassTile in ivk_patches.cu
 
 
 def build_dedup_tables(mesh, system, tables):
@@ -99,6 +104,14 @@ def build_dedup_tables(mesh, system, tables):
     rep = np.array(reps, dtype=np.int64)
     order = np.lexsort((np.arange(P), class_of))
     rep_nodes = [cn[t.node_off[q]:t.node_off[q + 1]] for q in rep]
+    cstart = np.concatenate([[0], np.cumsum(np.bincount(class_of, minlength=n_classes))])
+    starts, classes = [], []
+    for c in range(n_classes):
+        s = np.arange(cstart[c], cstart[c + 1], CLASS_TILE)
+        starts.append(s)
+        classes.append(np.full(len(s), c))
+    tile_start = np.concatenate(starts + [[P]]).astype(np.int64)
     return DedupTables(n_classes=n_classes, class_of=class_of,
                        perm=perm.astype(np.uint8), order=order, rep=rep,
-                       rep_nodes=rep_nodes, rep_vertex=t.order[rep])
+                       rep_nodes=rep_nodes, rep_vertex=t.order[rep],
+                       tile_start=tile_start, tile_class=np.concatenate(classes))

@@ -408,15 +408,24 @@ class VankaPatchSet:
             desc.kron = C.pointer(d["kron"])
         if self.dedup is not None:
             dd = self.dedup
-            d["class_of"] = upload(dd.class_of, np.int32)
-            d["perm"] = upload(dd.perm, np.uint8)
-            d["order"] = upload(dd.order, np.int32)
+            # canonical gather list and write positions, in tile (class) order
+            lens = t.sizes[dd.order].astype(np.int64)
+            starts = t.idx_off[dd.order].astype(np.int64)
+            cum = np.concatenate([[0], np.cumsum(lens)])
+            flat = np.repeat(starts - cum[:-1], lens) + np.arange(t.total_m)
+            le = np.repeat(starts, lens) + dd.perm[flat].astype(np.int64)
+            d["cidx"] = upload(t.idx[le], np.int32)
+            d["cdst"] = upload(slot_pos[le] if self.scatter == "owner" else le, np.int32)
+            d["class_off"] = upload(np.append(self.inv_off, self.inv_size), np.int64)
+            d["tile_start"] = upload(dd.tile_start, np.int32)
+            d["tile_class"] = upload(dd.tile_class, np.int32)
+            d["tile_off"] = upload(cum[dd.tile_start], np.int32)
             desc.n_classes = dd.n_classes
-            desc.class_of = d["class_of"].data_ptr()
-            desc.perm = d["perm"].data_ptr()
-            desc.order = d["order"].data_ptr()
-            desc.class_inv_off = d["inv_off"].data_ptr()
+            desc.class_inv_off = d["class_off"].data_ptr()
             desc.class_inv = d["inv"].data_ptr()
+            desc.n_tiles = len(dd.tile_class)
+            for name in ("tile_start", "tile_class", "tile_off", "cidx", "cdst"):
+                setattr(desc, name, d[name].data_ptr())
             # the class representatives as a patch set of their own (K7 input)
             sizes = t.sizes[dd.rep]
             rep_idx_off = np.concatenate([[0], np.cumsum(sizes)])
