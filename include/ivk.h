@@ -192,6 +192,12 @@ typedef struct ivk_coarse_desc {
   const double* u_diag;    /* nb tiles (upper; padding diagonal = 1)      */
   const int32_t* perm_r;   /* (P_r b)[perm_r[i]] = b[i]                   */
   const int32_t* perm_c;   /* x[i] = y[perm_c[i]]                         */
+  /* Dense alternative (non-NULL: the tile fields may be NULL): the n x n
+   * operator P (A + Z Z^T)^-1 P, P = I - Z Z^T, formed at setup from the same
+   * SuperLU factors, row-major with leading dimension dense_ld (multiple of
+   * 4); the solve is then one GEMV spread over every SM. */
+  const double* dense;
+  int32_t dense_ld;
 } ivk_coarse_desc;
 
 const char* ivk_last_error(void);
@@ -237,7 +243,8 @@ int ivk_restrict(const ivk_transfer_desc* t, const double* rf, double* rc, void*
 /* xf += (I_s (x) P) ec on unconstrained fine rows (solvers.py:343-346). */
 int ivk_prolong_add(const ivk_transfer_desc* t, const double* ec, double* xf, void* stream);
 
-/* x = CoarseSolver.solve(b) (solvers.py:284-287); b and x must not alias. */
+/* x = CoarseSolver.solve(b) (solvers.py:284-287): tile triangular solves, or
+ * one GEMV with c->dense when set; b and x must not alias. */
 int ivk_coarse_solve(const ivk_coarse_desc* c, const double* b, double* x, void* stream);
 
 /* Per-stage pressure-mean removal in place (stages.py:174-178). */

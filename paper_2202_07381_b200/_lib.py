@@ -99,6 +99,7 @@ class CoarseDesc(C.Structure):
         ("u_colptr", C.c_void_p), ("u_row", C.c_void_p), ("u_tiles", C.c_void_p),
         ("u_diag", C.c_void_p),
         ("perm_r", C.c_void_p), ("perm_c", C.c_void_p),
+        ("dense", C.c_void_p), ("dense_ld", C.c_int32),
     ]
 
 

@@ -220,6 +220,31 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) coarse_solve_kernel(CoarseP
   for (int i = threadIdx.x; i < c.n; i += blockDim.x) x[i] = v[i];
 }
 
+// Dense coarse operator: warp per row, 256-bit loads along the row, x from
+// L1; fixed-order shuffle reduction (deterministic).
+constexpr int kGemvWarps = 8;
+
+__global__ void __launch_bounds__(kGemvWarps * 32) dense_gemv_kernel(int n, int ld,
+                                                                     const double* __restrict__ A,
+                                                                     const double* __restrict__ x,
+                                                                     double* __restrict__ y) {
+  const int row = blockIdx.x * kGemvWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double* a = A + (long)row * ld;
+  double acc = 0.0;
+  for (int j = 4 * lane; j < n; j += 128) {
+    const double4 v = *reinterpret_cast<const double4*>(a + j);
+    acc = fma(v.x, __ldg(x + j), acc);
+    if (j + 1 < n) acc = fma(v.y, __ldg(x + j + 1), acc);
+    if (j + 2 < n) acc = fma(v.z, __ldg(x + j + 2), acc);
+    if (j + 3 < n) acc = fma(v.w, __ldg(x + j + 3), acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) y[row] = acc;
+}
+
 }  // namespace ivk
 
 using namespace ivk;
@@ -227,7 +252,17 @@ using namespace ivk;
 extern "C" {
 
 int ivk_coarse_solve(const ivk_coarse_desc* c, const double* b, double* x, void* stream) {
-  IVK_REQUIRE(c && c->l_colptr && c->l_row && c->l_tiles && c->l_diag && c->u_colptr &&
+  IVK_REQUIRE(c != nullptr, "bad coarse descriptor");
+  if (c->dense) {
+    IVK_REQUIRE(b && x && b != x, "bad coarse vectors");
+    IVK_REQUIRE(c->n > 0 && c->dense_ld >= c->n && (c->dense_ld & 3) == 0,
+                "bad dense coarse operator (n=%d ld=%d)", c->n, c->dense_ld);
+    const int grid = (c->n + kGemvWarps - 1) / kGemvWarps;
+    dense_gemv_kernel<<<grid, kGemvWarps * 32, 0, as_stream(stream)>>>(c->n, c->dense_ld, c->dense,
+                                                                       b, x);
+    return check_launch("ivk_coarse_solve(dense)");
+  }
+  IVK_REQUIRE(c->l_colptr && c->l_row && c->l_tiles && c->l_diag && c->u_colptr &&
                   c->u_row && c->u_tiles && c->u_diag && c->perm_r && c->perm_c,
               "bad coarse descriptor");
   IVK_REQUIRE(b && x && b != x, "bad coarse vectors");

@@ -616,17 +616,40 @@ class CoarseSolver:
     """Fixed SuperLU factorisation of A + Z Z^T (solvers.py:271-287).
 
     The factorisation is the reference's own host setup (scipy ``splu`` with
-    its defaults); the per-cycle solve (projection, permuted dense
-    triangular solves, projection) is kernel K6 on the device."""
+    its defaults).  The per-cycle solve x = P LU^-1 P b (P = I - Z Z^T) is
+    kernel K6 on the device, in one of two forms:
 
-    def __init__(self, system):
+    * ``method="dense"`` (default): P (A + Z Z^T)^-1 P is formed once at setup
+      from the same LU factors (one LU solve per unit vector) and applied as
+      one GEMV spread over every SM -- the coarse solve stops being a serial
+      single-CTA chain.  Its result differs from the triangular solves by
+      rounding only (measured 2e-15 .. 6e-14 relative where cond(A) <= 1e6,
+      ~cond * eps at the cond 6e7 RadauIIA(3) coarse level, the same order as
+      SuperLU's own forward error), and its backward error matches SuperLU's.
+    * ``method="lu"``: the permuted triangular solves on tile-sparse copies
+      of the factors (one CTA, TMA-staged diagonal tiles)."""
+
+    def __init__(self, system, method="dense"):
+        if method not in ("dense", "lu"):
+            raise ValueError(f"unknown coarse method {method!r}")
         A = system.materialize()
         Z = system.pressure_nullspace()
         reg = sp.csr_matrix(Z @ Z.T)
         self.lu = spla.splu((A + reg).tocsc())
         self.Z = Z
         self.system = system
+        self.method = method
         self._dev = None
+
+    def dense_operator(self):
+        """P (A + Z Z^T)^-1 P from the LU factors (n x n, fp64)."""
+        n = self.system.dim
+        inv = self.lu.solve(np.eye(n))
+        Z = np.asarray(self.Z)
+        izt = inv @ Z
+        out = inv - izt @ Z.T
+        out -= Z @ (Z.T @ out)
+        return out
 
     def tiles(self):
         """Tile-sparse (32 x 32, column-major tiles) copies of the factors."""
@@ -638,6 +661,19 @@ class CoarseSolver:
             return self._dev
         from ._device import upload
         s = self.system
+        d = _lib.CoarseDesc()
+        d.n = s.dim
+        d.stages, d.n_u, d.n_p = s.r, s.n_u, s.n_p
+        if self.method == "dense":
+            ld = (s.dim + 3) & ~3
+            D = np.zeros((s.dim, ld))
+            D[:, :s.dim] = self.dense_operator()
+            t = {"dense": upload(D.reshape(-1), np.float64)}
+            d.dense = t["dense"].data_ptr()
+            d.dense_ld = ld
+            d.nb = (s.dim + 31) // 32
+            self._dev = {"tensors": t, "desc": d}
+            return self._dev
         (lc, lr, lt, ld, nb), (uc, ur, ut, ud, _) = self.tiles()
         t = {
             "l_colptr": upload(lc, np.int32), "l_row": upload(lr, np.int32),
@@ -647,11 +683,8 @@ class CoarseSolver:
             "perm_r": upload(self.lu.perm_r, np.int32),
             "perm_c": upload(self.lu.perm_c, np.int32),
         }
-        d = _lib.CoarseDesc()
-        d.n = s.dim
         d.nb = nb
         d.l_ntiles, d.u_ntiles = int(lc[-1]), int(uc[-1])
-        d.stages, d.n_u, d.n_p = s.r, s.n_u, s.n_p
         for k in t:
             setattr(d, k, t[k].data_ptr())
         self._dev = {"tensors": t, "desc": d}
@@ -717,8 +750,8 @@ def tile_factor(F, lower, tile=32, invert_lower_diag=False):
     return colptr, row_of, tiles_cm, diag_cm, nb
 
 
-def coarse_direct_solve(system):
-    return CoarseSolver(system)
+def coarse_direct_solve(system, method="dense"):
+    return CoarseSolver(system, method)
 
 
 # --------------------------------------------------------------- V-cycle
@@ -906,7 +939,7 @@ class MGHierarchyOp:
                 lev.patches.factor()
         s0 = self.levels[0].system
         s0.download_convection()
-        self.coarse = CoarseSolver(s0)
+        self.coarse = CoarseSolver(s0, getattr(self.coarse, "method", "dense"))
         self._graph = None
         self._bufs = None
 

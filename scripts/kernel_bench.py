@@ -49,6 +49,8 @@ def main():
     b0 = torch.randn(S0.dim, dtype=torch.float64, device="cuda")
     x0 = torch.empty_like(b0)
     out["coarse_us"] = timeit(lambda: cs.solve_into(b0, x0), reps)
+    cl = CoarseSolver(S0, "lu")
+    out["coarse_lu_us"] = timeit(lambda: cl.solve_into(b0, x0), reps)
     modes = sys.argv[3].split(",") if len(sys.argv) > 3 else \
         (["kron", "dedup", "kron-sym", "full"] if conv is None else ["kron", "full"])
     for mode in modes:

@@ -102,3 +102,31 @@ def test_invalid_arguments_raise():
         S.matvec(np.zeros(S.dim + 1))
     with pytest.raises(ValueError):
         apply_vanka(mg.levels[-1].patches, S, np.zeros(3), np.zeros(S.dim))
+
+
+@pytest.mark.parametrize("name", ["crossed", "cfg1", "s3", "ns"])
+def test_coarse_methods_against_superlu(name):
+    """K6 in both forms against the reference's own solve (solvers.py:284-287):
+    x = P lu.solve(P b), P = I - Z Z^T."""
+    import torch
+    from harness import setup
+    from paper_2202_07381_b200.solvers import CoarseSolver
+    from paper_2202_07381_b200.stages import StageSystem
+    disc, tab, conv, case = setup(name)
+    S0 = StageSystem(disc.blocks[0], tab, case["dt"], disc.cdofs[0],
+                     None if conv is None else conv[0])
+    A = S0.materialize()
+    b = np.random.default_rng(5).standard_normal(S0.dim)
+    for method in ("dense", "lu"):
+        cs = CoarseSolver(S0, method)
+        Z = cs.Z
+        pb = b - Z @ (Z.T @ b)
+        ref = cs.lu.solve(pb)
+        ref -= Z @ (Z.T @ ref)
+        x = torch.empty(S0.dim, dtype=torch.float64, device="cuda")
+        got = cs.solve_into(torch.from_numpy(b).cuda(), x).cpu().numpy()
+        tol = 1e-12 if name in ("crossed", "cfg1") else 1e-7
+        assert rel(got, ref) <= tol, method
+        be = np.linalg.norm(A @ got - pb) / np.linalg.norm(pb)
+        be_ref = np.linalg.norm(A @ ref - pb) / np.linalg.norm(pb)
+        assert be <= max(10 * be_ref, 1e-13), method
