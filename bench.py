@@ -181,19 +181,62 @@ def cpu_sample(cfg, sample_patches=2048):
     return op, pat, b, w, scale, len(members), len(idxs)
 
 
-def time_cpu_sweep(op, pat, b, w, scale, reps=3):
-    """Seconds per full sweep (matvec full-size + sampled solve scaled)."""
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def threaded_solve_additive(pat, resid, pool, nthreads):
+    """The oracle's solve_additive (einsum + bincount per size group,
+    solvers.py:214-222) with each group's patches split over host threads
+    (numpy releases the GIL inside einsum/bincount); partial sums are added in
+    chunk order."""
+    n = len(resid)
+    z = np.zeros(n)
+
+    def chunk(args):
+        idx, inv = args
+        local = np.einsum("pij,pj->pi", inv, resid[idx])
+        return np.bincount(idx.ravel(), weights=local.ravel(), minlength=n)
+
+    for idx, inv in pat.groups:
+        P = len(idx)
+        k = max(1, min(nthreads, P // 16))
+        cuts = [(i * P) // k for i in range(k + 1)]
+        for part in pool.map(chunk, [(idx[a:b], inv[a:b]) for a, b in zip(cuts[:-1], cuts[1:])]):
+            z += part
+    return z
+
+
+def best_threads(op, pat, b, w, scale):
+    """All host threads, unless one thread is faster (small configs)."""
+    n = host_threads()
+    if n == 1:
+        return 1
+    t1 = time_cpu_sweep(op, pat, b, w, scale, reps=2, nthreads=1)[0]
+    tn = time_cpu_sweep(op, pat, b, w, scale, reps=2, nthreads=n)[0]
+    return n if tn < t1 else 1
+
+
+def time_cpu_sweep(op, pat, b, w, scale, reps=3, nthreads=None):
+    """Seconds per full sweep (matvec full-size + sampled solve scaled), the
+    patch solves spread over ``nthreads`` host threads."""
+    from concurrent.futures import ThreadPoolExecutor
+    nthreads = nthreads or host_threads()
     x = np.zeros(op.dim)
     best_mv, best_sa = np.inf, np.inf
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        r = b - op.matvec(x)
-        t1 = time.perf_counter()
-        z = pat.solve_additive(r)
-        t2 = time.perf_counter()
-        _ = x + 0.5 * w * z
-        best_mv = min(best_mv, t1 - t0)
-        best_sa = min(best_sa, t2 - t1)
+    with ThreadPoolExecutor(nthreads) as pool:
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            r = b - op.matvec(x)
+            t1 = time.perf_counter()
+            z = threaded_solve_additive(pat, r, pool, nthreads)
+            t2 = time.perf_counter()
+            _ = x + 0.5 * w * z
+            best_mv = min(best_mv, t1 - t0)
+            best_sa = min(best_sa, t2 - t1)
     return best_mv + scale * best_sa, best_mv, best_sa
 
 
@@ -202,15 +245,16 @@ def run_reference(args, rank, world):
         return
     cfg = CONFIGS[args.config]
     op, pat, b, w, scale, n_s, n_all = cpu_sample(cfg)
+    nth = best_threads(op, pat, b, w, scale)
     for _ in range(args.warmup):
-        time_cpu_sweep(op, pat, b, w, scale, reps=1)
+        time_cpu_sweep(op, pat, b, w, scale, reps=1, nthreads=nth)
     times = []
     for _ in range(args.steps):
-        t, _, _ = time_cpu_sweep(op, pat, b, w, scale, reps=1)
+        t, _, _ = time_cpu_sweep(op, pat, b, w, scale, reps=1, nthreads=nth)
         times.append(t)
     t = float(np.mean(times))
     sample = (f"full-size residual matvec + patch solves of {n_s} of {n_all} interior patches "
-              f"(scaled x{scale:.2f}) per step")
+              f"(scaled x{scale:.2f}) per step; patch solves on {nth} host threads")
     line = {"impl": "reference", "metric": metric_name(cfg), "value": 1.0 / t, "unit": "sweeps/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
@@ -218,7 +262,7 @@ def run_reference(args, rank, world):
             "config": {"workload": f"{cfg['name']} fine-level IRK-Vanka sweep (CPU oracle port)",
                        "problem": cfg["label"], "dim": op.dim},
             "stage_dof_updates_per_s": op.dim / t,
-            "cpu_baseline": {"value": 1.0 / t, "unit": "sweeps/s", "cores": 1, "kind": "port",
+            "cpu_baseline": {"value": 1.0 / t, "unit": "sweeps/s", "cores": nth, "kind": "port",
                              "sample": sample},
             "e2e": {"value": 1.0 / t, "unit": "sweeps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -451,14 +495,46 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     t_e2e = max_over_ranks(e_start.elapsed_time(e_stop) / 1e3 / args.steps, world)
 
+    # --shard (N > 1): one cfg2 problem strip-partitioned over the N ranks
+    # (shard.py): the fine-level sweep with its two NCCL halo exchanges,
+    # strong scaling, beside the replica headline
+    sharded = None
+    if world > 1 and args.shard:
+        from paper_2202_07381_b200.shard import (DeviceBackend, DistComm, ShardedSweep,
+                                                 StripPartition, shard_plans)
+        mesh = disc.fine_mesh
+        plans = shard_plans(S, mesh, StripPartition(mesh, world))
+        plan = plans[rank]
+        sw = ShardedSweep(plan, DeviceBackend(S, mesh, plan, mode=fine.mode,
+                                              weights=fine.pou_weights()), omega=0.5)
+        comm = DistComm()
+        xs = torch.zeros_like(b)
+        for _ in range(max(args.warmup, 3)):
+            sw.sweep(xs, b, comm)
+        torch.cuda.synchronize()
+        barrier(world)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(args.steps):
+            sw.sweep(xs, b, comm)
+        s1.record()
+        torch.cuda.synchronize()
+        t_sh = max_over_ranks(s0.elapsed_time(s1) / 1e3 / args.steps, world)
+        sharded = {"ms_per_sweep": 1e3 * t_sh, "sweeps_per_s": 1.0 / t_sh, "parts": world,
+                   "scaling": "strong", "partition": "vertex strips, (y, x) order",
+                   "rank0_exchange_doubles_per_sweep":
+                       int(sum(len(s) for s in plan.shared.values()) +
+                           sum(len(s) for s in plan.halo_send.values())) if rank == 0 else None}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         op, pat, bb, ww, scale, n_s, n_all = cpu_sample(cfg)
-        t_cpu, t_mv, t_sa = time_cpu_sweep(op, pat, bb, ww, scale, reps=3)
-        cpu = {"value": 1.0 / t_cpu, "unit": "sweeps/s", "cores": 1, "kind": "port",
-               "sample": (f"oracle: full-size residual matvec ({1e3 * t_mv:.0f} ms) + patch solves "
-                          f"of {n_s}/{n_all} interior patches ({1e3 * t_sa:.0f} ms, scaled "
-                          f"x{scale:.2f}); numpy einsum/bincount, single-threaded hot path")}
+        nth = best_threads(op, pat, bb, ww, scale)
+        t_cpu, t_mv, t_sa = time_cpu_sweep(op, pat, bb, ww, scale, reps=3, nthreads=nth)
+        cpu = {"value": 1.0 / t_cpu, "unit": "sweeps/s", "cores": nth, "kind": "port",
+               "sample": (f"oracle: full-size residual matvec ({1e3 * t_mv:.0f} ms, scipy, one "
+                          f"thread) + patch solves of {n_s}/{n_all} interior patches "
+                          f"({1e3 * t_sa:.0f} ms on {nth} threads, scaled x{scale:.2f})")}
 
     if rank == 0:
         line = {
@@ -500,6 +576,7 @@ def run_ours(args, rank, world, local):
             "vcycle_ms": vc,
             "fgmres": solves,
             "dedup_cycle": dedup,
+            "sharded": sharded,
             "setup_s": {"discretization": t_disc, "build_mg_gpu_factor": t_build,
                         "newton_relinearize": relin},
             "finite": finite,
@@ -516,6 +593,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2",
                     help="BASELINE config; cfg2 is the headline workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="N > 1: also time one problem strip-partitioned over the ranks")
     ap.add_argument("--no-full-mode", action="store_true",
                     help="skip timing the reference (full-inverse) formulation")
     args = ap.parse_args()

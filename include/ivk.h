@@ -224,6 +224,26 @@ int ivk_patch_combine(const ivk_patch_desc* pd, const double* local, const doubl
                       double alpha, double beta, const double* w, double* out,
                       double* accum, void* stream);
 
+/* Sharded sweep (shard.py): the same three kernels
+ * restricted to one rank's part of the fine level.
+ * ivk_stage_apply_slices: K1 on the listed warp slices only (velocity slice
+ *   s < ceil(n_nodes/16) covers nodes 16s..16s+15, pressure slice
+ *   ceil(n_nodes/16) + t covers P1 nodes 32t..32t+31); other rows of out
+ *   are untouched.
+ * ivk_patch_combine_list: K4 on the listed DoFs only.
+ * ivk_index_copy: dst[dst_idx[i]] = src[src_idx[i]] + beta * dst[dst_idx[i]]
+ *   (NULL index = identity) -- halo pack / unpack.
+ * ivk_index_update: out[d] = alpha x[d] + beta w[d] z[d] for d in idx. */
+int ivk_stage_apply_slices(const ivk_operator_desc* op, const int32_t* slices, int32_t n_slices,
+                           const double* x, const double* b, double* out, void* stream);
+int ivk_patch_combine_list(const ivk_patch_desc* pd, const int32_t* dofs, int32_t n_dofs,
+                           const double* local, const double* x, double alpha, double beta,
+                           const double* w, double* out, double* accum, void* stream);
+int ivk_index_copy(int64_t n, const int32_t* src_idx, const double* src, const int32_t* dst_idx,
+                   double* dst, double beta, void* stream);
+int ivk_index_update(int64_t n, const int32_t* idx, double alpha, const double* x, double beta,
+                     const double* w, const double* z, double* out, void* stream);
+
 /* Assemble every patch matrix from the operator (solvers.py:186-212) and
  * invert it in place into pd->inv (np.linalg.inv, solvers.py:177) by
  * Gauss-Jordan with partial pivoting.  *singular_dev (device int32, set to

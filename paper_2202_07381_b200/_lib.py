@@ -134,6 +134,11 @@ _SIGS = {
     "ivk_patch_combine": ([C.POINTER(PatchDesc), _P, _P, C.c_double, C.c_double, _P, _P, _P, _P],
                           C.c_int),
     "ivk_patch_factor": ([C.POINTER(OperatorDesc), C.POINTER(PatchDesc), _P, _P], C.c_int),
+    "ivk_stage_apply_slices": ([C.POINTER(OperatorDesc), _P, C.c_int32, _P, _P, _P, _P], C.c_int),
+    "ivk_patch_combine_list": ([C.POINTER(PatchDesc), _P, C.c_int32, _P, _P, C.c_double,
+                                C.c_double, _P, _P, _P, _P], C.c_int),
+    "ivk_index_copy": ([C.c_int64, _P, _P, _P, _P, C.c_double, _P], C.c_int),
+    "ivk_index_update": ([C.c_int64, _P, C.c_double, _P, C.c_double, _P, _P, _P, _P], C.c_int),
     "ivk_vanka_sweep": ([C.POINTER(OperatorDesc), C.POINTER(PatchDesc), _P, _P, C.c_double, _P,
                          _P, _P, _P, _P], C.c_int),
     "ivk_restrict": ([C.POINTER(TransferDesc), _P, _P, _P], C.c_int),

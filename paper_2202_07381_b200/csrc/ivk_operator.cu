@@ -59,12 +59,20 @@ struct OpParams {
 // Pressure rows: SELL-32, one thread per P1 node.  Entry e of a slice's
 // row j sits at ptr[slice] + H e + j (H = 16 / 32).
 // NC = 0 (Stokes), 1 (one J shared by all stages) or S (per-stage J_i).
-template <int S, int NC>
+// LIST: only the warps (slices) listed in `slices` run -- the rows a shard's
+// patches read (shard.py); the other rows of `out` are left untouched.
+template <int S, int NC, bool LIST>
 __global__ void __launch_bounds__(256) stage_apply_kernel(OpParams op, const double* __restrict__ x,
                                                           const double* __restrict__ b,
-                                                          double* __restrict__ out) {
+                                                          double* __restrict__ out,
+                                                          const int32_t* __restrict__ slices,
+                                                          int n_slices) {
   const int nslice_v = (op.n_nodes + 15) >> 4;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if constexpr (LIST) {
+    if (warp >= n_slices) return;
+    warp = __ldg(slices + warp);
+  }
   const int lane = threadIdx.x & 31;
   const int nu = 2 * op.n_nodes;
   const long sd = nu + op.n_p;
@@ -218,17 +226,27 @@ int validate_op(const ivk_operator_desc* d) {
 
 template <int S>
 static void launch_stage_apply(const OpParams& q, int nconv, const double* x, const double* b,
-                               double* out, cudaStream_t st) {
+                               double* out, const int32_t* slices, int n_slices,
+                               cudaStream_t st) {
   const OpParams& p = q;
-  const long warps = ((p.n_nodes + 15) >> 4) + ((p.n_p + 31) >> 5);
+  const long warps = slices ? n_slices : ((p.n_nodes + 15) >> 4) + ((p.n_p + 31) >> 5);
   const int block = 256;
   const int grid = (int)((warps * 32 + block - 1) / block);
+  if (slices) {
+    if (nconv == 0)
+      stage_apply_kernel<S, 0, true><<<grid, block, 0, st>>>(q, x, b, out, slices, n_slices);
+    else if (nconv == 1)
+      stage_apply_kernel<S, 1, true><<<grid, block, 0, st>>>(q, x, b, out, slices, n_slices);
+    else
+      stage_apply_kernel<S, S, true><<<grid, block, 0, st>>>(q, x, b, out, slices, n_slices);
+    return;
+  }
   if (nconv == 0)
-    stage_apply_kernel<S, 0><<<grid, block, 0, st>>>(q, x, b, out);
+    stage_apply_kernel<S, 0, false><<<grid, block, 0, st>>>(q, x, b, out, nullptr, 0);
   else if (nconv == 1)
-    stage_apply_kernel<S, 1><<<grid, block, 0, st>>>(q, x, b, out);
+    stage_apply_kernel<S, 1, false><<<grid, block, 0, st>>>(q, x, b, out, nullptr, 0);
   else
-    stage_apply_kernel<S, S><<<grid, block, 0, st>>>(q, x, b, out);
+    stage_apply_kernel<S, S, false><<<grid, block, 0, st>>>(q, x, b, out, nullptr, 0);
 }
 
 // ---------------------------------------------------------------- vectors
@@ -296,8 +314,8 @@ const char* ivk_last_error(void) { return g_err; }
 int ivk_version(void) { return 1; }
 int64_t ivk_launch_count(void) { return g_launches.load(); }
 
-int ivk_stage_apply(const ivk_operator_desc* op, const double* x, const double* b, double* out,
-                    void* stream) {
+static int stage_apply(const ivk_operator_desc* op, const int32_t* slices, int32_t n_slices,
+                       const double* x, const double* b, double* out, void* stream) {
   int rc = validate_op(op);
   if (rc) return rc;
   IVK_REQUIRE(x && out, "x/out is NULL");
@@ -305,11 +323,65 @@ int ivk_stage_apply(const ivk_operator_desc* op, const double* x, const double* 
   OpParams p = make_op_params(op);
   cudaStream_t st = as_stream(stream);
   switch (op->stages) {
-    case 1: launch_stage_apply<1>(p, op->n_conv, x, b, out, st); break;
-    case 2: launch_stage_apply<2>(p, op->n_conv, x, b, out, st); break;
-    case 3: launch_stage_apply<3>(p, op->n_conv, x, b, out, st); break;
+    case 1: launch_stage_apply<1>(p, op->n_conv, x, b, out, slices, n_slices, st); break;
+    case 2: launch_stage_apply<2>(p, op->n_conv, x, b, out, slices, n_slices, st); break;
+    case 3: launch_stage_apply<3>(p, op->n_conv, x, b, out, slices, n_slices, st); break;
   }
   return check_launch("ivk_stage_apply");
+}
+
+int ivk_stage_apply(const ivk_operator_desc* op, const double* x, const double* b, double* out,
+                    void* stream) {
+  return stage_apply(op, nullptr, 0, x, b, out, stream);
+}
+
+int ivk_stage_apply_slices(const ivk_operator_desc* op, const int32_t* slices, int32_t n_slices,
+                           const double* x, const double* b, double* out, void* stream) {
+  IVK_REQUIRE(slices != nullptr && n_slices >= 0, "bad slice list");
+  if (n_slices == 0) return IVK_OK;
+  return stage_apply(op, slices, n_slices, x, b, out, stream);
+}
+
+__global__ void index_copy_kernel(int64_t n, const int32_t* __restrict__ src_idx,
+                                  const double* __restrict__ src, const int32_t* __restrict__ dst_idx,
+                                  double* __restrict__ dst, double beta) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = src[src_idx ? src_idx[i] : i];
+    const int64_t o = dst_idx ? dst_idx[i] : i;
+    dst[o] = beta == 0.0 ? v : fma(beta, dst[o], v);
+  }
+}
+
+__global__ void index_update_kernel(int64_t n, const int32_t* __restrict__ idx, double alpha,
+                                    const double* __restrict__ x, double beta,
+                                    const double* __restrict__ w, const double* __restrict__ z,
+                                    double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int d = idx[i];
+    double v = beta * (w ? w[d] : 1.0) * z[d];
+    if (x) v = alpha * x[d] + v;
+    out[d] = v;
+  }
+}
+
+int ivk_index_copy(int64_t n, const int32_t* src_idx, const double* src, const int32_t* dst_idx,
+                   double* dst, double beta, void* stream) {
+  IVK_REQUIRE(n >= 0 && src && dst, "bad index_copy arguments");
+  if (n == 0) return IVK_OK;
+  index_copy_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, src_idx, src, dst_idx, dst,
+                                                                     beta);
+  return check_launch("ivk_index_copy");
+}
+
+int ivk_index_update(int64_t n, const int32_t* idx, double alpha, const double* x, double beta,
+                     const double* w, const double* z, double* out, void* stream) {
+  IVK_REQUIRE(n >= 0 && idx && z && out, "bad index_update arguments");
+  if (n == 0) return IVK_OK;
+  index_update_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, idx, alpha, x, beta, w,
+                                                                       z, out);
+  return check_launch("ivk_index_update");
 }
 
 int ivk_axpby(int64_t n, double alpha, const double* x, double beta, const double* y, double* out,

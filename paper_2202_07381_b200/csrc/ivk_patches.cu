@@ -167,10 +167,14 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kernel(PatchPara
 
 // -------------------------------------------------------------------- K4
 
+// dofs != NULL: only the listed DoFs (a shard's patch DoFs, shard.py).
 __global__ void patch_combine_kernel(PatchParams pd, const double* __restrict__ local,
                                      const double* x, double alpha, double beta,
-                                     const double* __restrict__ w, double* out, double* accum) {
-  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < pd.dim; d += gridDim.x * blockDim.x) {
+                                     const double* __restrict__ w, double* out, double* accum,
+                                     const int32_t* __restrict__ dofs, int n_dofs) {
+  const int n = dofs ? n_dofs : pd.dim;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int d = dofs ? dofs[i] : i;
     const int k0 = pd.dof_ptr[d], k1 = pd.dof_ptr[d + 1];
     double z = 0.0;
     if (pd.slot_pos) {
@@ -1265,16 +1269,32 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
   return check_launch("ivk_patch_apply");
 }
 
-int ivk_patch_combine(const ivk_patch_desc* pd, const double* local, const double* x, double alpha,
-                      double beta, const double* w, double* out, double* accum, void* stream) {
+static int patch_combine(const ivk_patch_desc* pd, const int32_t* dofs, int32_t n_dofs,
+                         const double* local, const double* x, double alpha, double beta,
+                         const double* w, double* out, double* accum, void* stream) {
   int rc = validate_patches(pd);
   if (rc) return rc;
   IVK_REQUIRE(local && out, "local/out is NULL");
   PatchParams p = make_patch_params(pd);
-  int grid = (pd->dim + 255) / 256;
+  const int n = dofs ? n_dofs : pd->dim;
+  if (n == 0) return IVK_OK;
+  int grid = (n + 255) / 256;
   if (grid > kSMs * 16) grid = kSMs * 16;
-  patch_combine_kernel<<<grid, 256, 0, as_stream(stream)>>>(p, local, x, alpha, beta, w, out, accum);
+  patch_combine_kernel<<<grid, 256, 0, as_stream(stream)>>>(p, local, x, alpha, beta, w, out, accum,
+                                                            dofs, n_dofs);
   return check_launch("ivk_patch_combine");
+}
+
+int ivk_patch_combine(const ivk_patch_desc* pd, const double* local, const double* x, double alpha,
+                      double beta, const double* w, double* out, double* accum, void* stream) {
+  return patch_combine(pd, nullptr, 0, local, x, alpha, beta, w, out, accum, stream);
+}
+
+int ivk_patch_combine_list(const ivk_patch_desc* pd, const int32_t* dofs, int32_t n_dofs,
+                           const double* local, const double* x, double alpha, double beta,
+                           const double* w, double* out, double* accum, void* stream) {
+  IVK_REQUIRE(dofs != nullptr && n_dofs >= 0, "bad DoF list");
+  return patch_combine(pd, dofs, n_dofs, local, x, alpha, beta, w, out, accum, stream);
 }
 
 int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int32_t* singular_dev,

@@ -76,8 +76,10 @@ def star_closure_nodes(mesh):
     return starts, (key % n_nodes).astype(np.int64)
 
 
-def build_patch_tables(mesh, n_nodes, n_p, stages, node_constrained):
-    """All host-side tables of the vertex-star patch set for one level."""
+def build_patch_tables(mesh, n_nodes, n_p, stages, node_constrained, vertices=None):
+    """All host-side tables of the vertex-star patch set for one level
+    (``vertices``: only those centre vertices' patches, in the same relative
+    group order)."""
     nv = mesh.num_vertices
     if n_p != nv:
         raise ValueError("mesh does not match the pressure space of the system")
@@ -95,20 +97,23 @@ def build_patch_tables(mesh, n_nodes, n_p, stages, node_constrained):
 
     # Group order: size ascending, vertex ascending (stable sort on size).
     order = np.argsort(size_of_v, kind="stable")
+    if vertices is not None:
+        keep = np.zeros(nv, dtype=bool)
+        keep[np.asarray(vertices, dtype=np.int64)] = True
+        order = order[keep[order]]
     sizes = size_of_v[order]
     kk = k_of_v[order]
     vstart = np.concatenate([[0], np.cumsum(k_of_v)])          # per-vertex node offsets
     # Node lists in flat patch order.
     node_off = np.concatenate([[0], np.cumsum(kk)])
-    gather = np.concatenate([np.arange(vstart[v], vstart[v + 1]) for v in order]) \
-        if nv < 64 else _ranges(vstart[order], kk)
+    gather = _ranges(vstart[order], kk)
     pnodes = nodes[gather]
 
     idx_off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
     total_m = int(idx_off[-1])
     idx = np.empty(total_m, dtype=np.int64)
     blk = 2 * kk + 1                                            # per-stage block length
-    P = nv
+    P = len(order)
     slot_of_node = np.repeat(np.arange(P), kk)                 # patch slot of each listed node
     alpha = np.arange(len(pnodes)) - node_off[slot_of_node]    # local node index
     for s in range(stages):

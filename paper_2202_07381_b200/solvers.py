@@ -221,15 +221,18 @@ class VankaPatchSet:
     convection Jacobian, A well diagonalisable, b <= 64), else full.
     """
 
-    def __init__(self, system, mesh, omega=1.0, factor=True, mode="auto", scatter="patch"):
+    def __init__(self, system, mesh, omega=1.0, factor=True, mode="auto", scatter="patch",
+                 vertices=None):
         if scatter not in ("patch", "owner"):
             raise ValueError(f"unknown scatter layout {scatter!r}")
         self.scatter = scatter
         self.omega = float(omega)
         self.system = system
-        self.num_patches = mesh.num_vertices
+        # vertices: only the patches of these centre vertices (one shard of a
+        # partitioned level, shard.py); None = every vertex
         self.tables = build_patch_tables(mesh, system.n_nodes, system.n_p, system.r,
-                                         system.node_constrained)
+                                         system.node_constrained, vertices=vertices)
+        self.num_patches = self.tables.num_patches
         if mode not in ("auto", "full", "kron", "kron-sym", "dedup"):
             raise ValueError(f"unknown patch mode {mode!r}")
         # kron-sym halves the inverse bytes but measures no faster than kron on
