@@ -72,6 +72,12 @@ __global__ void __launch_bounds__(256) stage_apply_kernel(OpParams op, const dou
   if constexpr (LIST) {
     if (warp >= n_slices) return;
     warp = __ldg(slices + warp);
+  } else {
+    // pressure slices (long rows: ~19 B^T entries per thread) first, so they
+    // do not form the last wave
+    const int npw = (op.n_p + 31) >> 5;
+    if (warp >= npw + nslice_v) return;  // grid padding (must not alias a slice: out may be b)
+    warp = warp < npw ? nslice_v + warp : warp - npw;
   }
   const int lane = threadIdx.x & 31;
   const int nu = 2 * op.n_nodes;
@@ -88,6 +94,34 @@ __global__ void __launch_bounds__(256) stage_apply_kernel(OpParams op, const dou
     for (int t = 0; t < ((NC > 1) ? S : 1); ++t) ju[t] = 0.0;
     if (!fixed) {
       const int e0 = op.p2_sptr[warp], e1 = op.p2_sptr[warp + 1];
+      if constexpr (NC == 0) {
+        // latency-bound gathers: U entries' (col, m/k) loads, then their 3 U
+        // x loads, in flight together (same summation order as one by one)
+        constexpr int U = 4;
+        for (int e = e0 + j; e < e1; e += 16 * U) {
+          int cl[U];
+          double2 mk[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int ee = e + 16 * u;
+            const bool ok = ee < e1;
+            cl[u] = ok ? op.p2_scol[ee] : -1;
+            mk[u] = ok ? op.p2_smk[ee] : make_double2(0.0, 0.0);
+          }
+          double uu[U][S];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int t = 0; t < S; ++t) uu[u][t] = cl[u] >= 0 ? x[t * sd + 2 * cl[u] + c] : 0.0;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int t = 0; t < S; ++t) {
+              mu[t] = fma(mk[u].x, uu[u][t], mu[t]);
+              ku[t] = fma(mk[u].y, uu[u][t], ku[t]);
+            }
+        }
+      } else
 #pragma unroll 2
       for (int e = e0 + j; e < e1; e += 16) {
         const int col = op.p2_scol[e];
@@ -127,12 +161,29 @@ __global__ void __launch_bounds__(256) stage_apply_kernel(OpParams op, const dou
         }
       }
       const int f0 = op.b_sptr[warp], f1 = op.b_sptr[warp + 1];
-      for (int e = f0 + j; e < f1; e += 16) {
-        const int q = op.b_scol[e];
-        const double2 bv = op.b_sval[e];
-        const double bc = c ? bv.y : bv.x;
+      {
+        constexpr int U = 4;
+        for (int e = f0 + j; e < f1; e += 16 * U) {
+          int q[U];
+          double bc[U];
 #pragma unroll
-        for (int t = 0; t < S; ++t) ku[t] = fma(bc, x[t * sd + nu + q], ku[t]);
+          for (int u = 0; u < U; ++u) {
+            const int ee = e + 16 * u;
+            const bool ok = ee < f1;
+            q[u] = ok ? op.b_scol[ee] : -1;
+            const double2 bv = ok ? op.b_sval[ee] : make_double2(0.0, 0.0);
+            bc[u] = c ? bv.y : bv.x;
+          }
+          double pp[U][S];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int t = 0; t < S; ++t) pp[u][t] = q[u] >= 0 ? x[t * sd + nu + q[u]] : 0.0;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int t = 0; t < S; ++t) ku[t] = fma(bc[u], pp[u][t], ku[t]);
+        }
       }
     }
     if (!valid) return;
@@ -159,15 +210,32 @@ __global__ void __launch_bounds__(256) stage_apply_kernel(OpParams op, const dou
 #pragma unroll
     for (int t = 0; t < S; ++t) btu[t] = 0.0;
     const int e0 = op.bt_sptr[ws], e1 = op.bt_sptr[ws + 1];
-#pragma unroll 2
-    for (int e = e0 + lane; e < e1; e += 32) {
-      const int n = op.bt_scol[e];
-      const double2 bv = op.bt_sval[e];
+    constexpr int U = 4;
+    for (int e = e0 + lane; e < e1; e += 32 * U) {
+      int nn[U];
+      double2 bv[U];
 #pragma unroll
-      for (int t = 0; t < S; ++t) {
-        btu[t] = fma(bv.x, x[t * sd + 2 * n], btu[t]);
-        btu[t] = fma(bv.y, x[t * sd + 2 * n + 1], btu[t]);
+      for (int u = 0; u < U; ++u) {
+        const int ee = e + 32 * u;
+        const bool ok = ee < e1;
+        nn[u] = ok ? op.bt_scol[ee] : -1;
+        bv[u] = ok ? op.bt_sval[ee] : make_double2(0.0, 0.0);
       }
+      double2 xv[U][S];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int t = 0; t < S; ++t)
+          // (stage offsets t * sd may be odd: no 16-byte vector loads)
+          xv[u][t] = nn[u] >= 0 ? make_double2(x[t * sd + 2 * nn[u]], x[t * sd + 2 * nn[u] + 1])
+                                : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          btu[t] = fma(bv[u].x, xv[u][t].x, btu[t]);
+          btu[t] = fma(bv[u].y, xv[u][t].y, btu[t]);
+        }
     }
     if (q >= op.n_p) return;
 #pragma unroll

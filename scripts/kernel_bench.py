@@ -54,7 +54,7 @@ def main():
     modes = sys.argv[3].split(",") if len(sys.argv) > 3 else \
         (["kron", "dedup", "kron-sym", "full"] if conv is None else ["kron", "full"])
     for mode in modes:
-        for scatter in ("patch",):
+        for scatter in (os.environ.get("KB_SCATTER", "patch").split(",")):
             pat = VankaPatchSet(S, disc.fine_mesh, mode=mode, scatter=scatter)
             dev = pat.device_data()
             w = pat.weights("pou")
