@@ -40,6 +40,12 @@ CONFIGS = {
     "cfg3": dict(name="cfg3", grid="diagonal", n0=8, level=6, mu=0.01, family="gauss",
                  stages=2, dt=1 / 512, seed=2, cheby_a=1.5, conv=True,
                  label="512x512 P2-P1 Oseen Re=100, Gauss(2), dt=1/512"),
+    # 3-D Stokes on Kuhn tetrahedra (fem3d.py): 4 levels 4^3 .. 32^3; the
+    # BASELINE smoother is PoU-weighted Vanka damped 0.4; unweighted 3-D
+    # Vanka's spectrum reaches ~17, so the Chebyshev interval is [4, 17]
+    "cfg4": dict(name="cfg4", grid="kuhn3d", n0=4, level=3, mu=1.0, family="radauiia",
+                 stages=2, dt=1 / 32, seed=3, cheby_a=4.0, cheby_b=17.0, omega=0.4,
+                 conv=False, label="32^3 Kuhn-tet P2-P1 3-D Stokes, RadauIIA(2), dt=1/32"),
 }
 
 
@@ -59,6 +65,10 @@ def metric_name(cfg):
 def make_disc(cfg):
     from paper_2202_07381_b200 import Discretization, tableau_lookup
     from paper_2202_07381_b200.discretization import oseen_convection
+    if cfg["grid"] == "kuhn3d":
+        from paper_2202_07381_b200.fem3d import Discretization3D
+        return (Discretization3D(cfg["n0"], cfg["level"], mu=cfg["mu"]),
+                tableau_lookup(cfg["family"], cfg["stages"]), None)
     disc = Discretization(cfg["n0"], cfg["level"], mu=cfg["mu"], grid=cfg["grid"])
     tab = tableau_lookup(cfg["family"], cfg["stages"])
     conv = oseen_convection(disc, cfg["stages"]) if cfg["conv"] else None
@@ -158,15 +168,17 @@ def cpu_sample(cfg, sample_patches=2048):
     of the sweep: the full-size residual matvec plus the patch solve of
     ``sample_patches`` interior patches, extrapolated to all patches."""
     from oracle.irk_vanka_oracle import OraclePatches, OracleStageOperator, oracle_patch_indices
-    from paper_2202_07381_b200.fem import velocity_boundary_dofs
     disc, tab, conv = make_disc(cfg)
     seed = cfg["seed"]
     blk = disc.blocks[-1]
     mesh = disc.fine_mesh
+    if blk.ncomp == 3:
+        sample_patches = min(sample_patches, 256)      # 392^2 inverses: keep it bounded
     cm = None if conv is None else [J.matrix for J in conv[-1]]
-    op = OracleStageOperator(blk.M, blk.K, blk.B, tab.A, cfg["dt"],
-                             velocity_boundary_dofs(mesh), convection=cm)
-    vels, idxs = oracle_patch_indices(mesh.cells, mesh.cell_to_edges, mesh.num_vertices, op)
+    op = OracleStageOperator(blk.M, blk.K, blk.B, tab.A, cfg["dt"], disc.cdofs[-1],
+                             convection=cm)
+    vels, idxs = oracle_patch_indices(mesh.cells, mesh.cell_to_edges, mesh.num_vertices, op,
+                                      ncomp=blk.ncomp)
     sizes = np.array([len(i) for i in idxs])
     interior = np.flatnonzero(sizes == sizes.max())
     rng = np.random.default_rng(0)
@@ -274,7 +286,7 @@ def run_reference(args, rank, world):
 def algorithmic_bytes(S, tables):
     """SURVEY.md §8(d) canonical bytes per sweep and per K3 launch."""
     nnz_s = len(S.blocks.col)
-    nnz_b = 2 * len(S.blocks.b_col)          # individual B values
+    nnz_b = S.nc * len(S.blocks.b_col)       # individual B values
     sm = tables.total_m
     sm2 = int(np.sum(tables.sizes.astype(np.int64) ** 2))
     sweep = 8 * (2 * nnz_s + nnz_b) + 4 * (nnz_s + nnz_b) + 8 * 3 * S.dim + 8 * sm2 + 4 * sm
@@ -295,15 +307,20 @@ def run_ours(args, rank, world, local):
     t_setup0 = time.perf_counter()
     disc, tab, conv = make_disc(cfg)
     t_disc = time.perf_counter() - t_setup0
-    cheb = SmootherSpec(pre=2, post=2, accel="chebyshev", cheby_a=cfg["cheby_a"], cheby_b=8.0)
+    cheb = SmootherSpec(pre=2, post=2, accel="chebyshev", cheby_a=cfg["cheby_a"],
+                        cheby_b=cfg.get("cheby_b", 8.0))
+    om = cfg.get("omega", 0.5)
+    is3d = cfg["grid"] == "kuhn3d"
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     # the headline sweep runs the general per-patch formulation (kron: every
-    # patch streams its own eigen-split inverse blocks from HBM)
-    mg, S = disc.build_mg(tab, cfg["dt"], cheb, convection=conv, patch_mode="kron")
+    # patch streams its own eigen-split inverse blocks from HBM; 3-D patches
+    # (b ~ 196) take the full per-patch inverse)
+    mg, S = disc.build_mg(tab, cfg["dt"], cheb, convection=conv,
+                          patch_mode="auto" if is3d else "kron")
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
-    pou = SmootherSpec(pre=2, post=2, accel="richardson", omega=0.5, weighting="pou")
+    pou = SmootherSpec(pre=2, post=2, accel="richardson", omega=om, weighting="pou")
     mg_pou = MGHierarchyOp([MGLevel(l.system, l.patches, pou, l.prolong) for l in mg.levels],
                            mg.coarse)
     fine = mg.levels[-1].patches
@@ -329,7 +346,7 @@ def run_ours(args, rank, world, local):
             _lib.check(L.ivk_patch_apply(dev["desc"], ptr(r), ptr(dev["local"]), st), "K3")
             if ev is not None:
                 ev[1].record()
-            _lib.check(L.ivk_patch_combine(dev["desc"], ptr(dev["local"]), ptr(x), 1.0, 0.5,
+            _lib.check(L.ivk_patch_combine(dev["desc"], ptr(dev["local"]), ptr(x), 1.0, om,
                                            ptr(w), ptr(x), None, st), "K4")
 
         for _ in range(warmup):
@@ -410,7 +427,7 @@ def run_ours(args, rank, world, local):
     # Translation-invariant dedup (Stokes on a uniform mesh): the same cycle
     # with patches sharing bitwise-identical class inverses.
     dedup = None
-    if conv is None and not args.no_full_mode:
+    if conv is None and not is3d and not args.no_full_mode:
         mg_d, _ = disc.build_mg(tab, cfg["dt"], cheb, convection=conv, patch_mode="dedup")
         mg_dp = MGHierarchyOp([MGLevel(l.system, l.patches, pou, l.prolong)
                                for l in mg_d.levels], mg_d.coarse)
@@ -434,7 +451,7 @@ def run_ours(args, rank, world, local):
                                 "inverse_bytes": 8 * fine.inv_size}}
     if not args.no_full_mode:
         from paper_2202_07381_b200 import VankaPatchSet
-        others = ["dedup", "kron-sym", "full"] if conv is None else ["full"]
+        others = [] if is3d else (["dedup", "kron-sym", "full"] if conv is None else ["full"])
         for other in others:
             if other == fine.mode:
                 continue
@@ -471,7 +488,7 @@ def run_ours(args, rank, world, local):
                 done[s].synchronize()       # host slot s is free again
             xd[s].copy_(xh[s], non_blocking=True)
             bd[s].copy_(bh[s], non_blocking=True)
-            apply_vanka(fine, S, xd[s], bd[s], omega=0.5, weights="pou", workspace=wss[s],
+            apply_vanka(fine, S, xd[s], bd[s], omega=om, weights="pou", workspace=wss[s],
                         out=yd[s])
             outh[s].copy_(yd[s], non_blocking=True)
             ev = torch.cuda.Event()
@@ -542,9 +559,9 @@ def run_ours(args, rank, world, local):
             "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded uniform[-1,1] RHS, BASELINE config 2)",
+            "data": f"synthetic (seeded uniform[-1,1] RHS, BASELINE {cfg['name']})",
             "config": {"workload": f"{cfg['name']} fine-level IRK-Vanka sweep (K1->K3->K4), "
-                                   "PoU w=0.5",
+                                   f"PoU w={om}",
                        "problem": cfg["label"], "patch_formulation": fine.mode,
                        "levels": disc.num_levels, "dt": cfg["dt"], "dim": S.dim,
                        "patches": fine.num_patches,

@@ -79,6 +79,11 @@ typedef struct ivk_operator_desc {
   const int32_t* bt_sptr;   /* ceil(n_p/32) + 1                            */
   const int32_t* bt_scol;
   const double* bt_sval;
+  /* Velocity components per scalar node: 0 or 2 (2-D, as above), or 3 (3-D
+   * Kuhn tetrahedra, fem3d.py: n_u = 3 n_nodes, B/B^T values are (B_x, B_y,
+   * B_z) triples, velocity rows in SELL-32 with one thread per node; no
+   * convection). */
+  int32_t ncomp;
 } ivk_operator_desc;
 
 /* Vanka vertex-star patch set (solvers.py:116-222).  Patches are laid out
@@ -168,6 +173,7 @@ typedef struct ivk_transfer_desc {
   const int32_t *p1t_rowptr, *p1t_col; const double* p1t_val;
   const uint8_t* fine_constrained;   /* per fine scalar node            */
   const uint8_t* coarse_constrained; /* per coarse scalar node          */
+  int32_t ncomp;                     /* velocity components (0/2, or 3) */
 } ivk_transfer_desc;
 
 /* Coarsest-level direct solve with fixed LU factors (CoarseSolver,
@@ -275,7 +281,7 @@ int ivk_axpby(int64_t n, double alpha, const double* x, double beta, const doubl
               double* out, void* stream);
 /* out = 0 except out[d] = src[d] on constrained velocity DoFs (the z[cd] = r[cd]
  * seeding of MGHierarchyOp.precondition, solvers.py:352-354). */
-int ivk_seed_constrained(int32_t stages, int32_t n_nodes, int32_t n_p,
+int ivk_seed_constrained(int32_t stages, int32_t n_nodes, int32_t ncomp, int32_t n_p,
                          const uint8_t* node_constrained, const double* src,
                          double* out, void* stream);
 

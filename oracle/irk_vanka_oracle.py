@@ -132,8 +132,9 @@ class OracleStageOperator:
         return (out + sp.diags(ones)).tocsr()
 
 
-def oracle_patch_indices(cells, cell_to_edges, num_vertices, op):
-    """Per-vertex patch index lists (solvers.py:132-166), loop form."""
+def oracle_patch_indices(cells, cell_to_edges, num_vertices, op, ncomp=2):
+    """Per-vertex patch index lists (solvers.py:132-166), loop form
+    (``ncomp`` = 3 for the 3-D tetrahedral extension)."""
     V = num_vertices
     cell_nodes = np.hstack([cells, V + cell_to_edges])
     closure = [set() for _ in range(V)]
@@ -146,9 +147,9 @@ def oracle_patch_indices(cells, cell_to_edges, num_vertices, op):
     vels, idxs = [], []
     for v in range(V):
         sn = np.array(sorted(closure[v]), dtype=np.int64)
-        vel = np.empty(2 * len(sn), dtype=np.int64)
-        vel[0::2] = 2 * sn
-        vel[1::2] = 2 * sn + 1
+        vel = np.empty(ncomp * len(sn), dtype=np.int64)
+        for d in range(ncomp):
+            vel[d::ncomp] = ncomp * sn + d
         vel = vel[~cmask[vel]]
         vels.append(vel)
         idxs.append(np.concatenate([np.concatenate([s * sd + vel, [s * sd + n_u + v]])

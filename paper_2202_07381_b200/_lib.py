@@ -45,6 +45,7 @@ class OperatorDesc(C.Structure):
         ("conv_s", C.c_void_p), ("nnz_s", C.c_int32),
         ("b_sptr", C.c_void_p), ("b_scol", C.c_void_p), ("b_sval", C.c_void_p),
         ("bt_sptr", C.c_void_p), ("bt_scol", C.c_void_p), ("bt_sval", C.c_void_p),
+        ("ncomp", C.c_int32),
     ]
 
 
@@ -87,6 +88,7 @@ class TransferDesc(C.Structure):
         ("p1_rowptr", C.c_void_p), ("p1_col", C.c_void_p), ("p1_val", C.c_void_p),
         ("p1t_rowptr", C.c_void_p), ("p1t_col", C.c_void_p), ("p1t_val", C.c_void_p),
         ("fine_constrained", C.c_void_p), ("coarse_constrained", C.c_void_p),
+        ("ncomp", C.c_int32),
     ]
 
 
@@ -146,7 +148,8 @@ _SIGS = {
     "ivk_coarse_solve": ([C.POINTER(CoarseDesc), _P, _P, _P], C.c_int),
     "ivk_project_pressure_means": ([C.c_int32, C.c_int32, C.c_int32, _P, _P], C.c_int),
     "ivk_axpby": ([C.c_int64, C.c_double, _P, C.c_double, _P, _P, _P], C.c_int),
-    "ivk_seed_constrained": ([C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P], C.c_int),
+    "ivk_seed_constrained": ([C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P],
+                             C.c_int),
     "ivk_convection_assemble": ([C.POINTER(ConvectionDesc), _P, _P, _P, _P, _P, _P], C.c_int),
     "ivk_dot": ([C.c_int64, _P, _P, _P, _P], C.c_int),
     "ivk_norm": ([C.c_int64, _P, _P, _P], C.c_int),

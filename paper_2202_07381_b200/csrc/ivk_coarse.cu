@@ -233,12 +233,23 @@ __global__ void __launch_bounds__(kGemvWarps * 32) dense_gemv_kernel(int n, int 
   if (row >= n) return;
   const double* a = A + (long)row * ld;
   double acc = 0.0;
-  for (int j = 4 * lane; j < n; j += 128) {
-    const double4 v = *reinterpret_cast<const double4*>(a + j);
-    acc = fma(v.x, __ldg(x + j), acc);
-    if (j + 1 < n) acc = fma(v.y, __ldg(x + j + 1), acc);
-    if (j + 2 < n) acc = fma(v.z, __ldg(x + j + 2), acc);
-    if (j + 3 < n) acc = fma(v.w, __ldg(x + j + 3), acc);
+  // 4 x 32 B of the row in flight per lane (few rows: latency, not bandwidth)
+  constexpr int U = 4;
+  for (int j0 = 4 * lane; j0 < n; j0 += 128 * U) {
+    double4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + 128 * u;
+      v[u] = j < n ? *reinterpret_cast<const double4*>(a + j) : make_double4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + 128 * u;
+      if (j < n) acc = fma(v[u].x, __ldg(x + j), acc);
+      if (j + 1 < n) acc = fma(v[u].y, __ldg(x + j + 1), acc);
+      if (j + 2 < n) acc = fma(v[u].z, __ldg(x + j + 2), acc);
+      if (j + 3 < n) acc = fma(v[u].w, __ldg(x + j + 3), acc);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

@@ -278,6 +278,8 @@ int validate_op(const ivk_operator_desc* d) {
   IVK_REQUIRE(d->stages >= 1 && d->stages <= IVK_MAX_STAGES, "stages=%d outside [1,%d]", d->stages,
               IVK_MAX_STAGES);
   IVK_REQUIRE(d->n_nodes > 0 && d->n_p > 0, "empty operator");
+  IVK_REQUIRE(d->ncomp == 0 || d->ncomp == 2 || d->ncomp == 3, "ncomp must be 2 or 3");
+  IVK_REQUIRE(d->ncomp != 3 || d->n_conv == 0, "3-D operators carry no convection");
   IVK_REQUIRE(d->n_conv == 0 || d->n_conv == 1 || d->n_conv == d->stages,
               "n_conv must be 0, 1 or stages");
   IVK_REQUIRE(d->n_conv == 0 || d->conv != nullptr, "conv is NULL with n_conv > 0");
@@ -292,14 +294,144 @@ int validate_op(const ivk_operator_desc* d) {
   return IVK_OK;
 }
 
+// 3-D (ncomp = 3, Kuhn tetrahedra): velocity rows in SELL-32, one thread per
+// scalar node for its 3 components and all S stages; B / B^T values are
+// (B_x, B_y, B_z) triples.  Pressure rows as in 2-D.
+template <int S, bool LIST>
+__global__ void __launch_bounds__(256) stage_apply3_kernel(OpParams op, const double* __restrict__ x,
+                                                           const double* __restrict__ b,
+                                                           double* __restrict__ out,
+                                                           const int32_t* __restrict__ slices,
+                                                           int n_slices) {
+  const int nslice_v = (op.n_nodes + 31) >> 5;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if constexpr (LIST) {
+    if (warp >= n_slices) return;
+    warp = __ldg(slices + warp);
+  } else {
+    const int npw = (op.n_p + 31) >> 5;
+    if (warp >= npw + nslice_v) return;
+    warp = warp < npw ? nslice_v + warp : warp - npw;
+  }
+  const int lane = threadIdx.x & 31;
+  const int nu = 3 * op.n_nodes;
+  const long sd = nu + op.n_p;
+  const double* bsv = reinterpret_cast<const double*>(op.b_sval);
+  const double* btv = reinterpret_cast<const double*>(op.bt_sval);
+  if (warp < nslice_v) {
+    const int n = (warp << 5) + lane;
+    const bool valid = n < op.n_nodes;
+    const bool fixed = valid && op.cmask[n];
+    double mu[S][3], ku[S][3];
+#pragma unroll
+    for (int t = 0; t < S; ++t)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) mu[t][d] = ku[t][d] = 0.0;
+    if (!fixed) {
+      const int e0 = op.p2_sptr[warp], e1 = op.p2_sptr[warp + 1];
+      constexpr int U = 2;
+      for (int e = e0 + lane; e < e1; e += 32 * U) {
+        int cl[U];
+        double2 mk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int ee = e + 32 * u;
+          const bool ok = ee < e1;
+          cl[u] = ok ? op.p2_scol[ee] : -1;
+          mk[u] = ok ? op.p2_smk[ee] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (cl[u] < 0) continue;
+#pragma unroll
+          for (int t = 0; t < S; ++t)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const double v = x[t * sd + 3 * cl[u] + d];
+              mu[t][d] = fma(mk[u].x, v, mu[t][d]);
+              ku[t][d] = fma(mk[u].y, v, ku[t][d]);
+            }
+        }
+      }
+      const int f0 = op.b_sptr[warp], f1 = op.b_sptr[warp + 1];
+      for (int e = f0 + lane; e < f1; e += 32) {
+        const int q = op.b_scol[e];
+        const double bx = bsv[3L * e], by = bsv[3L * e + 1], bz = bsv[3L * e + 2];
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          const double pv = x[t * sd + nu + q];
+          ku[t][0] = fma(bx, pv, ku[t][0]);
+          ku[t][1] = fma(by, pv, ku[t][1]);
+          ku[t][2] = fma(bz, pv, ku[t][2]);
+        }
+      }
+    }
+    if (!valid) return;
+#pragma unroll
+    for (int i = 0; i < S; ++i)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const long o = i * sd + 3L * n + d;
+        double y;
+        if (fixed) {
+          y = x[o];
+        } else {
+          double acc = 0.0;
+#pragma unroll
+          for (int t = 0; t < S; ++t) acc += op.a[i * S + t] * ku[t][d];
+          y = mu[i][d] + op.dt * acc;
+        }
+        out[o] = b ? b[o] - y : y;
+      }
+  } else {
+    const int ws = warp - nslice_v;
+    const int q = (ws << 5) + lane;
+    if (ws >= ((op.n_p + 31) >> 5)) return;
+    double btu[S];
+#pragma unroll
+    for (int t = 0; t < S; ++t) btu[t] = 0.0;
+    const int e0 = op.bt_sptr[ws], e1 = op.bt_sptr[ws + 1];
+    for (int e = e0 + lane; e < e1; e += 32) {
+      const int nn = op.bt_scol[e];
+      const double bx = btv[3L * e], by = btv[3L * e + 1], bz = btv[3L * e + 2];
+#pragma unroll
+      for (int t = 0; t < S; ++t) {
+        const double* xv = x + t * sd + 3L * nn;
+        btu[t] = fma(bx, xv[0], btu[t]);
+        btu[t] = fma(by, xv[1], btu[t]);
+        btu[t] = fma(bz, xv[2], btu[t]);
+      }
+    }
+    if (q >= op.n_p) return;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t < S; ++t) acc += op.a[i * S + t] * btu[t];
+      const double y = op.dt * acc;
+      const long o = i * sd + nu + q;
+      out[o] = b ? b[o] - y : y;
+    }
+  }
+}
+
 template <int S>
-static void launch_stage_apply(const OpParams& q, int nconv, const double* x, const double* b,
-                               double* out, const int32_t* slices, int n_slices,
+static void launch_stage_apply(const OpParams& q, int nconv, int ncomp, const double* x,
+                               const double* b, double* out, const int32_t* slices, int n_slices,
                                cudaStream_t st) {
   const OpParams& p = q;
-  const long warps = slices ? n_slices : ((p.n_nodes + 15) >> 4) + ((p.n_p + 31) >> 5);
+  const int node_rows = ncomp == 3 ? 32 : 16;
+  const long warps = slices ? n_slices
+                            : (p.n_nodes + node_rows - 1) / node_rows + ((p.n_p + 31) >> 5);
   const int block = 256;
   const int grid = (int)((warps * 32 + block - 1) / block);
+  if (ncomp == 3) {
+    if (slices)
+      stage_apply3_kernel<S, true><<<grid, block, 0, st>>>(q, x, b, out, slices, n_slices);
+    else
+      stage_apply3_kernel<S, false><<<grid, block, 0, st>>>(q, x, b, out, nullptr, 0);
+    return;
+  }
   if (slices) {
     if (nconv == 0)
       stage_apply_kernel<S, 0, true><<<grid, block, 0, st>>>(q, x, b, out, slices, n_slices);
@@ -351,15 +483,17 @@ __global__ void __launch_bounds__(1024) project_means_kernel(int n_u, int n_p, d
   for (int i = threadIdx.x; i < n_p; i += blockDim.x) p[i] -= mean;
 }
 
-__global__ void seed_constrained_kernel(int S, int n_nodes, int n_p, const uint8_t* __restrict__ cm,
+__global__ void seed_constrained_kernel(int S, int n_nodes, int nc, int n_p,
+                                        const uint8_t* __restrict__ cm,
                                         const double* __restrict__ src, double* __restrict__ out) {
-  const long sd = 2L * n_nodes + n_p;
+  const long nu = (long)nc * n_nodes;
+  const long sd = nu + n_p;
   const long total = S * sd;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
        i += (long)gridDim.x * blockDim.x) {
     const long loc = i % sd;
     double v = 0.0;
-    if (loc < 2L * n_nodes && cm[loc >> 1]) v = src[i];
+    if (loc < nu && cm[loc / nc]) v = src[i];
     out[i] = v;
   }
 }
@@ -391,9 +525,9 @@ static int stage_apply(const ivk_operator_desc* op, const int32_t* slices, int32
   OpParams p = make_op_params(op);
   cudaStream_t st = as_stream(stream);
   switch (op->stages) {
-    case 1: launch_stage_apply<1>(p, op->n_conv, x, b, out, slices, n_slices, st); break;
-    case 2: launch_stage_apply<2>(p, op->n_conv, x, b, out, slices, n_slices, st); break;
-    case 3: launch_stage_apply<3>(p, op->n_conv, x, b, out, slices, n_slices, st); break;
+    case 1: launch_stage_apply<1>(p, op->n_conv, op->ncomp, x, b, out, slices, n_slices, st); break;
+    case 2: launch_stage_apply<2>(p, op->n_conv, op->ncomp, x, b, out, slices, n_slices, st); break;
+    case 3: launch_stage_apply<3>(p, op->n_conv, op->ncomp, x, b, out, slices, n_slices, st); break;
   }
   return check_launch("ivk_stage_apply");
 }
@@ -466,12 +600,13 @@ int ivk_project_pressure_means(int32_t stages, int32_t n_u, int32_t n_p, double*
   return check_launch("ivk_project_pressure_means");
 }
 
-int ivk_seed_constrained(int32_t stages, int32_t n_nodes, int32_t n_p, const uint8_t* cm,
-                         const double* src, double* out, void* stream) {
-  IVK_REQUIRE(cm && src && out && stages >= 1, "bad seed arguments");
-  const long total = (long)stages * (2L * n_nodes + n_p);
-  seed_constrained_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(stages, n_nodes, n_p,
-                                                                              cm, src, out);
+int ivk_seed_constrained(int32_t stages, int32_t n_nodes, int32_t ncomp, int32_t n_p,
+                         const uint8_t* cm, const double* src, double* out, void* stream) {
+  IVK_REQUIRE(cm && src && out && stages >= 1 && (ncomp == 2 || ncomp == 3),
+              "bad seed arguments");
+  const long total = (long)stages * ((long)ncomp * n_nodes + n_p);
+  seed_constrained_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
+      stages, n_nodes, ncomp, n_p, cm, src, out);
   return check_launch("ivk_seed_constrained");
 }
 

@@ -212,6 +212,8 @@ struct FactorParams {
   const int32_t* __restrict__ b_rowptr;
   const int32_t* __restrict__ b_col;
   const double2* __restrict__ b_val;
+  const double* __restrict__ b_raw;  // ncomp values per entry
+  int ncomp;
 };
 
 static FactorParams make_factor_params(const ivk_operator_desc* op) {
@@ -230,6 +232,8 @@ static FactorParams make_factor_params(const ivk_operator_desc* op) {
   f.b_rowptr = op->b_rowptr;
   f.b_col = op->b_col;
   f.b_val = reinterpret_cast<const double2*>(op->b_val);
+  f.b_raw = op->b_val;
+  f.ncomp = op->ncomp == 3 ? 3 : 2;
   return f;
 }
 
@@ -380,6 +384,137 @@ __global__ void __launch_bounds__(kFactorThreads) patch_factor_kernel(FactorPara
   }
 }
 
+
+// Patches too large for shared memory (3-D: d = s (3k + 1) ~ 400): one CTA
+// per patch (persistent), the matrix held in its own slot of the inverse
+// store.  The TRANSPOSE A^T is assembled (row-major, leading dimension ld)
+// and inverted in place by Gauss-Jordan with row pivoting -- (A^T)^-1 =
+// (A^-1)^T is exactly the Inv^T layout K3 streams, so no scratch and no
+// final transpose.  Pivot row and multiplier column are staged in shared
+// memory each step; the d x d update streams through L2.
+constexpr int kFactorGlobalThreads = 1024;
+
+template <int NC>
+__global__ void __launch_bounds__(kFactorGlobalThreads) patch_factor_global_kernel(
+    FactorParams op, PatchParams pd, int32_t* singular) {
+  __shared__ double prow[512];
+  __shared__ double colk[512];
+  __shared__ int piv[512];
+  __shared__ int s_prow, s_bad;
+  const int tid = threadIdx.x;
+  const int S = op.S;
+  for (int p = blockIdx.x; p < pd.num_patches; p += gridDim.x) {
+    const int n0 = pd.node_off[p], nk = pd.node_off[p + 1] - n0;
+    const int* nodes = pd.node + n0;
+    const int v = pd.vertex[p];
+    const int mv = NC * nk, blk = mv + 1, d = S * blk;
+    const int ld = (d + 3) & ~3;
+    double* B = pd.inv + pd.inv_off[p];  // B[r * ld + c] = A[c][r]
+    for (int e = tid; e < d * ld; e += blockDim.x) B[e] = 0.0;
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    for (int pr = tid; pr < nk * nk; pr += blockDim.x) {
+      const int al = pr / nk, be = pr % nk;
+      const int row = nodes[al];
+      const int pos = find_col(op.p2_col, op.p2_rowptr[row], op.p2_rowptr[row + 1], nodes[be]);
+      if (pos < 0) continue;
+      const double2 mk = op.p2_mk[pos];
+      for (int a = 0; a < S; ++a)
+        for (int b = 0; b < S; ++b) {
+          const double f = op.dt * op.a[a * S + b];
+          const double val = (a == b ? mk.x : 0.0) + f * mk.y;
+          for (int cc = 0; cc < NC; ++cc) {
+            const int r = a * blk + NC * al + cc, col = b * blk + NC * be + cc;
+            B[(long)col * ld + r] = val;
+          }
+        }
+    }
+    for (int al = tid; al < nk; al += blockDim.x) {
+      const int row = nodes[al];
+      const int pos = find_col(op.b_col, op.b_rowptr[row], op.b_rowptr[row + 1], v);
+      for (int cc = 0; cc < NC; ++cc) {
+        const double bv = pos >= 0 ? op.b_raw[(long)pos * NC + cc] : 0.0;
+        for (int a = 0; a < S; ++a)
+          for (int b = 0; b < S; ++b) {
+            const double f = op.dt * op.a[a * S + b];
+            const int r = a * blk + NC * al + cc;
+            B[(long)(b * blk + mv) * ld + r] = f * bv;   // A[r][b*blk + mv]
+            B[(long)(b * blk + NC * al + cc) * ld + a * blk + mv] = f * bv;  // A[a*blk+mv][.]
+          }
+      }
+    }
+    __syncthreads();
+    for (int k = 0; k < d; ++k) {
+      if (tid < 32) {
+        double best = -1.0;
+        int bi = k;
+        for (int i = k + tid; i < d; i += 32) {
+          const double a = fabs(B[(long)i * ld + k]);
+          if (a > best) { best = a; bi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_down_sync(0xffffffffu, best, o);
+          const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (tid == 0) {
+          s_prow = bi;
+          piv[k] = bi;
+          if (!(best > 0.0)) s_bad = 1;
+        }
+      }
+      __syncthreads();
+      if (s_bad) break;
+      const int pr = s_prow;
+      // pivot row (swapped in) scaled, and the multiplier column
+      const double pinv = 1.0 / B[(long)pr * ld + k];
+      for (int j = tid; j < d; j += blockDim.x) {
+        const double t = B[(long)pr * ld + j];
+        prow[j] = (j == k) ? pinv : t * pinv;
+      }
+      for (int i = tid; i < d; i += blockDim.x)
+        colk[i] = (i == pr) ? B[(long)k * ld + k] : B[(long)i * ld + k];
+      __syncthreads();
+      // row pr <- old row k (the swap); then every row i != k updated
+      if (pr != k)
+        for (int j = tid; j < d; j += blockDim.x) B[(long)pr * ld + j] = B[(long)k * ld + j];
+      __syncthreads();
+      {
+        const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+        for (int i = warp; i < d; i += nw) {
+          double* arow = B + (long)i * ld;
+          const double f = colk[i];
+          if (i == k) {
+            for (int j = lane; j < d; j += 32) arow[j] = prow[j];
+          } else {
+            for (int j = lane; j < d; j += 32) {
+              const double base = (j == k) ? 0.0 : arow[j];
+              arow[j] = base - f * prow[j];
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (s_bad) {
+      if (tid == 0) atomicMin(singular, v);
+      __syncthreads();
+      continue;
+    }
+    for (int k = d - 1; k >= 0; --k) {
+      const int pk = piv[k];
+      if (pk != k) {
+        for (int i = tid; i < d; i += blockDim.x) {
+          const double t = B[(long)i * ld + k];
+          B[(long)i * ld + k] = B[(long)i * ld + pk];
+          B[(long)i * ld + pk] = t;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
 
 // ---------------------------------------------------------- Kronecker split
 //
@@ -1337,9 +1472,18 @@ int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int3
     return IVK_EUNSUPPORTED;
   }
   const size_t smem = (size_t)dmax * dmax * sizeof(double);
-  if (smem > 220 * 1024) {
-    set_error("ivk_patch_factor: patch size %d needs %zu B shared memory", dmax, smem);
-    return IVK_EUNSUPPORTED;
+  if (op->ncomp == 3 || smem > 220 * 1024) {
+    IVK_REQUIRE(op->n_conv == 0, "large-patch factorisation supports no convection");
+    FactorParams f = make_factor_params(op);
+    PatchParams p = make_patch_params(pd);
+    int grid = pd->num_patches < 128 ? pd->num_patches : 128;  // ~L2-resident working set
+    if (f.ncomp == 3)
+      patch_factor_global_kernel<3><<<grid, kFactorGlobalThreads, 0, as_stream(stream)>>>(
+          f, p, singular_dev);
+    else
+      patch_factor_global_kernel<2><<<grid, kFactorGlobalThreads, 0, as_stream(stream)>>>(
+          f, p, singular_dev);
+    return check_launch("ivk_patch_factor(global)");
   }
   cudaError_t e = cudaFuncSetAttribute(patch_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

@@ -42,6 +42,8 @@ def build_dedup_tables(mesh, system, tables):
     """Classes of bitwise-identical canonical patch matrices for ``tables``."""
     if system.convection is not None:
         raise ValueError("dedup needs a translation-invariant (convection-free) operator")
+    if system.nc != 2:
+        raise ValueError("dedup is implemented for 2-D levels")
     t = tables
     P = t.num_patches
     S = t.stages

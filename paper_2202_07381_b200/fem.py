@@ -122,11 +122,16 @@ class StokesBlocks:
     k: np.ndarray
     b_rowptr: np.ndarray
     b_col: np.ndarray
-    b_val: np.ndarray  # (nnz_b, 2)
+    b_val: np.ndarray  # (nnz_b, ncomp): (B_x, B_y) in 2-D, (B_x, B_y, B_z) in 3-D
+
+    @property
+    def ncomp(self):
+        """Velocity components per scalar node (2; 3 for fem3d)."""
+        return int(self.b_val.shape[1])
 
     @property
     def n_u(self):
-        return 2 * self.n_nodes
+        return self.ncomp * self.n_nodes
 
     @classmethod
     def from_vector(cls, M, K, B):
@@ -171,20 +176,19 @@ class StokesBlocks:
 
     @property
     def M(self):
-        return sp.kron(self.scalar_matrix(self.m), sp.identity(2), format="csr")
+        return sp.kron(self.scalar_matrix(self.m), sp.identity(self.ncomp), format="csr")
 
     @property
     def K(self):
-        return sp.kron(self.scalar_matrix(self.k), sp.identity(2), format="csr")
+        return sp.kron(self.scalar_matrix(self.k), sp.identity(self.ncomp), format="csr")
 
     @property
     def B(self):
-        nb = len(self.b_col)
+        nc = self.ncomp
         rows = np.repeat(np.arange(self.n_nodes), np.diff(self.b_rowptr))
-        r = np.concatenate([2 * rows, 2 * rows + 1])
-        c = np.concatenate([self.b_col, self.b_col]).astype(np.int64)
-        v = np.concatenate([self.b_val[:, 0], self.b_val[:, 1]])
-        assert len(v) == 2 * nb
+        r = np.concatenate([nc * rows + d for d in range(nc)])
+        c = np.concatenate([self.b_col] * nc).astype(np.int64)
+        v = np.concatenate([self.b_val[:, d] for d in range(nc)])
         return sp.csr_matrix((v, (r, c)), shape=(self.n_u, self.n_p))
 
 

@@ -64,19 +64,20 @@ class PatchTables:
 
 def star_closure_nodes(mesh):
     """CSR (starts, nodes): sorted unique scalar P2 nodes of the cells around
-    each vertex (solvers.py:135-145)."""
+    each vertex (solvers.py:135-145); triangles or tetrahedra."""
     nv = mesh.num_vertices
     n_nodes = nv + mesh.num_edges
-    cell_nodes = np.hstack([mesh.cells, nv + mesh.cell_to_edges])          # (C, 6)
-    centre = np.repeat(mesh.cells, 6, axis=1).reshape(-1)                  # (C*18,)
-    nodes = np.tile(cell_nodes, (1, 3)).reshape(-1)
+    cell_nodes = np.hstack([mesh.cells, nv + mesh.cell_to_edges])          # (C, 6 or 10)
+    nvc, nnc = mesh.cells.shape[1], cell_nodes.shape[1]
+    centre = np.repeat(mesh.cells, nnc, axis=1).reshape(-1)
+    nodes = np.tile(cell_nodes, (1, nvc)).reshape(-1)
     key = np.unique(centre.astype(np.int64) * n_nodes + nodes)
     v = key // n_nodes
     starts = np.concatenate([[0], np.cumsum(np.bincount(v, minlength=nv))])
     return starts, (key % n_nodes).astype(np.int64)
 
 
-def build_patch_tables(mesh, n_nodes, n_p, stages, node_constrained, vertices=None):
+def build_patch_tables(mesh, n_nodes, n_p, stages, node_constrained, vertices=None, ncomp=2):
     """All host-side tables of the vertex-star patch set for one level
     (``vertices``: only those centre vertices' patches, in the same relative
     group order)."""
@@ -85,7 +86,8 @@ def build_patch_tables(mesh, n_nodes, n_p, stages, node_constrained, vertices=No
         raise ValueError("mesh does not match the pressure space of the system")
     if n_nodes != nv + mesh.num_edges:
         raise ValueError("mesh does not match the velocity space of the system")
-    n_u = 2 * n_nodes
+    nc = int(ncomp)
+    n_u = nc * n_nodes
     sd = n_u + n_p
     dim = stages * sd
     starts, nodes = star_closure_nodes(mesh)
@@ -93,7 +95,7 @@ def build_patch_tables(mesh, n_nodes, n_p, stages, node_constrained, vertices=No
     free = ~node_constrained[nodes]
     nodes, owner = nodes[free], owner[free]
     k_of_v = np.bincount(owner, minlength=nv)                   # free nodes per vertex
-    size_of_v = stages * (2 * k_of_v + 1)
+    size_of_v = stages * (nc * k_of_v + 1)
 
     # Group order: size ascending, vertex ascending (stable sort on size).
     order = np.argsort(size_of_v, kind="stable")
@@ -112,16 +114,16 @@ def build_patch_tables(mesh, n_nodes, n_p, stages, node_constrained, vertices=No
     idx_off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
     total_m = int(idx_off[-1])
     idx = np.empty(total_m, dtype=np.int64)
-    blk = 2 * kk + 1                                            # per-stage block length
+    blk = nc * kk + 1                                           # per-stage block length
     P = len(order)
     slot_of_node = np.repeat(np.arange(P), kk)                 # patch slot of each listed node
     alpha = np.arange(len(pnodes)) - node_off[slot_of_node]    # local node index
     for s in range(stages):
         base = idx_off[:-1] + s * blk                          # start of stage block s
-        pos = base[slot_of_node] + 2 * alpha
-        idx[pos] = s * sd + 2 * pnodes
-        idx[pos + 1] = s * sd + 2 * pnodes + 1
-        idx[base + 2 * kk] = s * sd + n_u + order
+        pos = base[slot_of_node] + nc * alpha
+        for d in range(nc):
+            idx[pos + d] = s * sd + nc * pnodes + d
+        idx[base + nc * kk] = s * sd + n_u + order
     ld = (sizes + 3) & ~3
     blocks = sizes.astype(np.int64) * ld
     inv_off = np.concatenate([[0], np.cumsum(blocks)]).astype(np.int64)

@@ -88,6 +88,8 @@ def _node_dofs(system, nodes, pres):
 def shard_plans(system, mesh, partition):
     """Every rank's plan (identical on all ranks: pure function of the global
     tables)."""
+    if system.nc != 2:
+        raise ValueError("the sharded sweep is implemented for 2-D levels")
     t = build_patch_tables(mesh, system.n_nodes, system.n_p, system.r, system.node_constrained)
     part = partition.part
     N = partition.nparts

@@ -231,7 +231,8 @@ class VankaPatchSet:
         # vertices: only the patches of these centre vertices (one shard of a
         # partitioned level, shard.py); None = every vertex
         self.tables = build_patch_tables(mesh, system.n_nodes, system.n_p, system.r,
-                                         system.node_constrained, vertices=vertices)
+                                         system.node_constrained, vertices=vertices,
+                                         ncomp=system.nc)
         self.num_patches = self.tables.num_patches
         if mode not in ("auto", "full", "kron", "kron-sym", "dedup"):
             raise ValueError(f"unknown patch mode {mode!r}")
@@ -258,7 +259,7 @@ class VankaPatchSet:
                 if mode in ("kron", "kron-sym", "dedup"):
                     raise
                 self.kron = None
-        if self.kron is not None and (mode == "dedup" or (mode == "auto" and
+        if self.kron is not None and (mode == "dedup" or (mode == "auto" and system.nc == 2 and
                                                            system.convection is None)):
             # translation-invariant operator: share inverses between patches
             # whose canonical matrices are bitwise identical (dedup.py); "auto"
@@ -920,7 +921,7 @@ class MGHierarchyOp:
         from ._device import ptr, stream
         sys_ = self.finest
         dev = sys_.device_data()
-        _lib.check(_lib.lib().ivk_seed_constrained(sys_.r, sys_.n_nodes, sys_.n_p,
+        _lib.check(_lib.lib().ivk_seed_constrained(sys_.r, sys_.n_nodes, sys_.nc, sys_.n_p,
                                                    ptr(dev["tensors"]["cmask"]), ptr(r), ptr(z),
                                                    stream()), "seed_constrained")
         self._cycle(len(self.levels) - 1, z, r)

@@ -69,6 +69,7 @@ class StageSystem:
         self.tableau = tableau
         self.dt = float(dt)
         self.n_nodes = blocks.n_nodes
+        self.nc = blocks.ncomp          # velocity components per scalar node (2; 3 in 3-D)
         self.n_u = blocks.n_u
         self.n_p = blocks.n_p
         self.r = tableau.r
@@ -78,20 +79,23 @@ class StageSystem:
                                       dtype=np.int64)
         if convection is not None and len(convection) != self.r:
             raise ValueError("one convection Jacobian per stage required")
+        if convection is not None and self.nc != 2:
+            raise ValueError("convection is implemented for 2-D operators only")
 
         c = self.constrained
         node_mask = np.zeros(self.n_nodes, dtype=bool)
         if len(c):
             if c.min() < 0 or c.max() >= self.n_u:
                 raise ValueError("constrained DoF out of range")
-            nodes = np.unique(c // 2)
-            full = np.sort(np.concatenate([2 * nodes, 2 * nodes + 1]))
+            nc = self.nc
+            nodes = np.unique(c // nc)
+            full = np.sort(np.concatenate([nc * nodes + d for d in range(nc)]))
             if not np.array_equal(full, np.unique(c)):
                 raise ValueError("both velocity components of a constrained node must be "
                                  "constrained (node-level Dirichlet elimination)")
             node_mask[nodes] = True
         self.node_constrained = node_mask
-        self._cmask = np.repeat(node_mask, 2)
+        self._cmask = np.repeat(node_mask, self.nc)
 
         # Elimination D A D / D B (stages.py:77-85, fem.py:304-315), on the
         # scalar pattern: zero every entry touching a constrained node.
@@ -167,17 +171,18 @@ class StageSystem:
 
     @property
     def M(self):
-        return sp.kron(self._scalar(self._m), sp.identity(2), format="csr")
+        return sp.kron(self._scalar(self._m), sp.identity(self.nc), format="csr")
 
     @property
     def K(self):
-        return sp.kron(self._scalar(self._k), sp.identity(2), format="csr")
+        return sp.kron(self._scalar(self._k), sp.identity(self.nc), format="csr")
 
     @property
     def B(self):
-        r = np.concatenate([2 * self._brows, 2 * self._brows + 1])
-        c = np.concatenate([self.blocks.b_col, self.blocks.b_col]).astype(np.int64)
-        v = np.concatenate([self._b[:, 0], self._b[:, 1]])
+        nc = self.nc
+        r = np.concatenate([nc * self._brows + d for d in range(nc)])
+        c = np.concatenate([self.blocks.b_col] * nc).astype(np.int64)
+        v = np.concatenate([self._b[:, d] for d in range(nc)])
         return sp.csr_matrix((v, (r, c)), shape=(self.n_u, self.n_p))
 
     @property
@@ -251,9 +256,12 @@ class StageSystem:
             t["conv"] = upload(np.stack(self._conv_vals).reshape(len(self._conv_vals), -1, 4),
                                np.float64)
             n_conv = len(self._conv_vals)
-        # SELL-32 copies for the K1 apply (coalesced entry loads).
+        # SELL copies for the K1 apply (coalesced entry loads): velocity rows
+        # in slices of 16 nodes (2-D: lane pairs per node) or 32 (3-D: one
+        # thread per node), pressure rows in slices of 32.
+        cv = 16 if self.nc == 2 else 32
         sptr, scol, smk = to_sell(b.rowptr, b.col, np.column_stack([self._m, self._k]),
-                                  self.n_nodes, C=16)
+                                  self.n_nodes, C=cv)
         t["p2_sptr"], t["p2_scol"] = upload(sptr, np.int32), upload(scol, np.int32)
         t["p2_smk"] = upload(smk, np.float64)
         nnz_s = len(scol)
@@ -261,7 +269,7 @@ class StageSystem:
             cs = [to_sell(b.rowptr, b.col, v.reshape(-1, 4), self.n_nodes, C=16)[2]
                   for v in self._conv_vals]
             t["conv_s"] = upload(np.stack(cs), np.float64)
-        sptr, scol, sval = to_sell(b.b_rowptr, b.b_col, self._b, self.n_nodes, pad_col=0, C=16)
+        sptr, scol, sval = to_sell(b.b_rowptr, b.b_col, self._b, self.n_nodes, pad_col=0, C=cv)
         t["b_sptr"], t["b_scol"], t["b_sval"] = (upload(sptr, np.int32), upload(scol, np.int32),
                                                  upload(sval, np.float64))
         sptr, scol, sval = to_sell(bt_rowptr, self._brows[order], self._b[order], self.n_p,
@@ -295,6 +303,7 @@ class StageSystem:
             setattr(desc, k, t[k].data_ptr())
         desc.conv_s = t["conv_s"].data_ptr() if "conv_s" in t else None
         desc.nnz_s = nnz_s
+        desc.ncomp = self.nc
         self._dev = {"tensors": t, "desc": desc,
                      "cmask_dofs": torch.from_numpy(self._cmask).to(t["cmask"].device)}
         return self._dev

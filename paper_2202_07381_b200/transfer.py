@@ -1,4 +1,4 @@
-"""Stage prolongation I_s (x) blockdiag(P_P2 (x) I_2, P_P1) on the device.
+"""Stage prolongation I_s (x) blockdiag(P_P2 (x) I_d, P_P1) on the device (d = 2, or 3 in 3-D).
 
 Mirror of the reference ``Discretization.stage_prolong`` (bench.py:187-194)
 with the restriction ``P^T r`` and the constrained-row zeroing of
@@ -17,12 +17,13 @@ __all__ = ["StageTransfer"]
 
 
 class StageTransfer:
-    def __init__(self, p2, p1, stages, fine_node_constrained, coarse_node_constrained):
+    def __init__(self, p2, p1, stages, fine_node_constrained, coarse_node_constrained, ncomp=2):
         self.p2 = sp.csr_matrix(p2)
         self.p1 = sp.csr_matrix(p1)
         self.p2.sort_indices()
         self.p1.sort_indices()
         self.stages = int(stages)
+        self.ncomp = int(ncomp)
         self.nf_nodes, self.nc_nodes = self.p2.shape
         self.nf_p, self.nc_p = self.p1.shape
         self.fine_cm = np.asarray(fine_node_constrained, dtype=bool)
@@ -31,14 +32,14 @@ class StageTransfer:
 
     @property
     def shape(self):
-        sf = 2 * self.nf_nodes + self.nf_p
-        sc = 2 * self.nc_nodes + self.nc_p
+        sf = self.ncomp * self.nf_nodes + self.nf_p
+        sc = self.ncomp * self.nc_nodes + self.nc_p
         return (self.stages * sf, self.stages * sc)
 
     @property
     def matrix(self):
         """Reference-layout CSR (bench.py:187-194), for the oracle / API."""
-        P = sp.block_diag([sp.kron(self.p2, sp.identity(2)), self.p1]).tocsr()
+        P = sp.block_diag([sp.kron(self.p2, sp.identity(self.ncomp)), self.p1]).tocsr()
         return sp.kron(sp.identity(self.stages), P, format="csr")
 
     def device_data(self):
@@ -68,6 +69,7 @@ class StageTransfer:
                 setattr(d, f"{name}_{f}", t[f"{name}_{f}"].data_ptr())
         d.fine_constrained = t["fcm"].data_ptr()
         d.coarse_constrained = t["ccm"].data_ptr()
+        d.ncomp = self.ncomp
         self._dev = {"tensors": t, "desc": d}
         return self._dev
 
