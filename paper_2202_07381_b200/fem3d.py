@@ -203,8 +203,10 @@ class Discretization3D:
                                                      self.cnodes[level - 1], ncomp=3)
         return self._stage_prolong[key]
 
-    def build_mg(self, tableau, dt, smoother, mg_levels=None, use_graph=False,
+    def build_mg(self, tableau, dt, smoother, mg_levels=None, convection=None, use_graph=False,
                  patch_mode="auto"):
         from .discretization import Discretization
+        if convection is not None:
+            raise ValueError("3-D operators carry no convection")
         return Discretization.build_mg(self, tableau, dt, smoother, mg_levels=mg_levels,
                                        use_graph=use_graph, patch_mode=patch_mode)
