@@ -46,6 +46,12 @@ CONFIGS = {
     "cfg4": dict(name="cfg4", grid="kuhn3d", n0=4, level=3, mu=1.0, family="radauiia",
                  stages=2, dt=1 / 32, seed=3, cheby_a=4.0, cheby_b=17.0, omega=0.4,
                  conv=False, label="32^3 Kuhn-tet P2-P1 3-D Stokes, RadauIIA(2), dt=1/32"),
+    # 2-D resistive MHD, Newton-linearised (mhd.py): (u, B) vector P2, (p, r)
+    # P1, 128x128, Re = Rm = 100, S = 1; general operator path (K1g/K7g/K5g)
+    "cfg5": dict(name="cfg5", grid="mhd", n0=8, level=4, Re=100.0, Rm=100.0, S=1.0,
+                 family="radauiia", stages=2, dt=1 / 128, seed=4, cheby_a=2.0, omega=0.5,
+                 conv=False, label="128x128 P2/P2-P1/P1 resistive MHD Re=Rm=100, "
+                                   "RadauIIA(2), dt=1/128"),
 }
 
 
@@ -65,6 +71,11 @@ def metric_name(cfg):
 def make_disc(cfg):
     from paper_2202_07381_b200 import Discretization, tableau_lookup
     from paper_2202_07381_b200.discretization import oseen_convection
+    if cfg["grid"] == "mhd":
+        from paper_2202_07381_b200.mhd import MHDDiscretization, MHDParams
+        return (MHDDiscretization(cfg["n0"], cfg["level"],
+                                  MHDParams(cfg["Re"], cfg["Rm"], cfg["S"])),
+                tableau_lookup(cfg["family"], cfg["stages"]), None)
     if cfg["grid"] == "kuhn3d":
         from paper_2202_07381_b200.fem3d import Discretization3D
         return (Discretization3D(cfg["n0"], cfg["level"], mu=cfg["mu"]),
@@ -170,6 +181,8 @@ def cpu_sample(cfg, sample_patches=2048):
     from oracle.irk_vanka_oracle import OraclePatches, OracleStageOperator, oracle_patch_indices
     disc, tab, conv = make_disc(cfg)
     seed = cfg["seed"]
+    if cfg["grid"] == "mhd":
+        return cpu_sample_general(disc, tab, cfg, min(sample_patches, 512))
     blk = disc.blocks[-1]
     mesh = disc.fine_mesh
     if blk.ncomp == 3:
@@ -191,6 +204,32 @@ def cpu_sample(cfg, sample_patches=2048):
     w = np.ones(op.dim)
     scale = len(idxs) / len(members)
     return op, pat, b, w, scale, len(members), len(idxs)
+
+
+def cpu_sample_general(disc, tab, cfg, sample_patches):
+    """The general-operator oracle (oracle/general_oracle.py) on the same
+    bounded sample: full-size residual plus sampled interior patch solves."""
+    import scipy.sparse as sp
+    from oracle.general_oracle import (OracleGeneralOperator, OracleGeneralPatches,
+                                       oracle_general_patch_indices)
+    o = disc.ops[-1]
+    n_nodes, nv, n1 = o["layout"]
+    M = sp.csr_matrix((o["m"], o["col"], o["rowptr"]), shape=(n1, n1))
+    Lm = sp.csr_matrix((o["l"], o["col"], o["rowptr"]), shape=(n1, n1))
+    op = OracleGeneralOperator(M, Lm, tab.A, cfg["dt"], np.flatnonzero(o["cmask"]), n1 - nv)
+    mesh = disc.fine_mesh
+    idxs = oracle_general_patch_indices(mesh.cells, mesh.cell_to_edges, mesh.num_vertices, op,
+                                        4, 2)
+    sizes = np.array([len(i) for i in idxs])
+    interior = np.flatnonzero(sizes == sizes.max())
+    rng = np.random.default_rng(0)
+    members = np.sort(rng.choice(interior, size=min(sample_patches, len(interior)),
+                                 replace=False))
+    pat = OracleGeneralPatches(op, idxs, members=members)
+    b = np.random.default_rng(cfg["seed"]).uniform(-1, 1, op.dim)
+    b[op.constrained_stage_dofs()] = 0.0
+    op.project_pressure_means(b)
+    return op, pat, b, np.ones(op.dim), len(idxs) / len(members), len(members), len(idxs)
 
 
 def host_threads():
@@ -284,12 +323,18 @@ def run_reference(args, rank, world):
 # ----------------------------------------------------------------- GPU arm
 
 def algorithmic_bytes(S, tables):
-    """SURVEY.md §8(d) canonical bytes per sweep and per K3 launch."""
-    nnz_s = len(S.blocks.col)
-    nnz_b = S.nc * len(S.blocks.b_col)       # individual B values
+    """SURVEY.md §8(d) canonical bytes per sweep and per K3 launch.  General
+    operators (MHD): one (m, l) pair + int32 column per single-stage CSR
+    entry in place of the scalar (m, k) / B values."""
     sm = tables.total_m
     sm2 = int(np.sum(tables.sizes.astype(np.int64) ** 2))
-    sweep = 8 * (2 * nnz_s + nnz_b) + 4 * (nnz_s + nnz_b) + 8 * 3 * S.dim + 8 * sm2 + 4 * sm
+    if getattr(S, "general", False):
+        nnz = len(S.col)
+        sweep = 16 * nnz + 4 * nnz + 8 * 3 * S.dim + 8 * sm2 + 4 * sm
+    else:
+        nnz_s = len(S.blocks.col)
+        nnz_b = S.nc * len(S.blocks.b_col)       # individual B values
+        sweep = 8 * (2 * nnz_s + nnz_b) + 4 * (nnz_s + nnz_b) + 8 * 3 * S.dim + 8 * sm2 + 4 * sm
     # K3: inverses once, gather list, gathered r (each DoF once), local[] written
     k3 = 8 * sm2 + 4 * sm + 8 * S.dim + 8 * sm + 4 * (tables.num_patches + 1) \
         + 8 * tables.num_patches
@@ -311,6 +356,7 @@ def run_ours(args, rank, world, local):
                         cheby_b=cfg.get("cheby_b", 8.0))
     om = cfg.get("omega", 0.5)
     is3d = cfg["grid"] == "kuhn3d"
+    is_mhd = cfg["grid"] == "mhd"
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     # the headline sweep runs the general per-patch formulation (kron: every
@@ -338,9 +384,11 @@ def run_ours(args, rank, world, local):
         r = torch.zeros_like(b)
         w = pat.weights("pou")
 
+        k1 = L.ivk_general_apply if is_mhd else L.ivk_stage_apply
+
         def sweep(ev=None):
             st = stream()
-            _lib.check(L.ivk_stage_apply(S.desc, ptr(x), ptr(b), ptr(r), st), "K1")
+            _lib.check(k1(S.desc, ptr(x), ptr(b), ptr(r), st), "K1")
             if ev is not None:
                 ev[0].record()
             _lib.check(L.ivk_patch_apply(dev["desc"], ptr(r), ptr(dev["local"]), st), "K3")
@@ -427,7 +475,7 @@ def run_ours(args, rank, world, local):
     # Translation-invariant dedup (Stokes on a uniform mesh): the same cycle
     # with patches sharing bitwise-identical class inverses.
     dedup = None
-    if conv is None and not is3d and not args.no_full_mode:
+    if conv is None and not is3d and not is_mhd and not args.no_full_mode:
         mg_d, _ = disc.build_mg(tab, cfg["dt"], cheb, convection=conv, patch_mode="dedup")
         mg_dp = MGHierarchyOp([MGLevel(l.system, l.patches, pou, l.prolong)
                                for l in mg_d.levels], mg_d.coarse)
@@ -451,7 +499,8 @@ def run_ours(args, rank, world, local):
                                 "inverse_bytes": 8 * fine.inv_size}}
     if not args.no_full_mode:
         from paper_2202_07381_b200 import VankaPatchSet
-        others = [] if is3d else (["dedup", "kron-sym", "full"] if conv is None else ["full"])
+        others = [] if is3d else (["full"] if (is_mhd or conv is not None)
+                                  else ["dedup", "kron-sym", "full"])
         for other in others:
             if other == fine.mode:
                 continue

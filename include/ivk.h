@@ -336,6 +336,67 @@ int ivk_scale(int64_t n, const double* x, const double* coef, int32_t k, double*
 int ivk_lincomb(int64_t n, const double* Z, int64_t ldz, int32_t k, const double* y, double* x,
                 void* stream);
 
+/* ---- General stage-coupled operator (multi-field systems: BASELINE config 5
+ * MHD, mhd.py / general.py) -------------------------------------------------
+ * The stage system of any spatial operator shared by all stages,
+ *   I_s (x) M + dt A (x) L,
+ * with M and L given on ONE single-stage CSR pattern as (m, l) pairs, and
+ * identity rows on constrained single-stage DoFs (whose rows and columns the
+ * caller has already zeroed -- Dirichlet elimination as stages.py:77-85).
+ * This is StageSystem.matvec (stages.py:110-126) with the reference's
+ * [[M + dt a K, dt a B], [dt a B^T, 0]] structure replaced by a general L.
+ * Vectors are stage-major [x_1, ..., x_s], x_i of length n. */
+typedef struct ivk_general_desc {
+  int32_t stages;
+  int32_t n;                /* single-stage DoFs                            */
+  int32_t nnz;              /* CSR entries                                  */
+  double dt;
+  double butcher_a[IVK_MAX_STAGES * IVK_MAX_STAGES];
+  const int32_t* rowptr;    /* n + 1, columns sorted per row (K7g)          */
+  const int32_t* col;
+  const double* ml;         /* nnz * 2: (m, l)                              */
+  const int32_t* sptr;      /* SELL-32 copy for K1g: ceil(n/32) + 1         */
+  const int32_t* scol;      /* padding: column = the row, values 0          */
+  const double* sml;
+  const uint8_t* constrained; /* n                                          */
+} ivk_general_desc;
+
+/* Single-stage transfer P (fine x coarse CSR) and its explicit transpose,
+ * applied as I_s (x) P (bench.py:187-194 generalised to any field layout). */
+typedef struct ivk_general_transfer_desc {
+  int32_t stages;
+  int32_t nf, nc;           /* single-stage fine / coarse DoFs              */
+  const int32_t *p_rowptr, *p_col; const double* p_val;     /* nf rows      */
+  const int32_t *pt_rowptr, *pt_col; const double* pt_val;  /* nc rows      */
+  const uint8_t* fine_constrained;   /* nf                                  */
+  const uint8_t* coarse_constrained; /* nc                                  */
+} ivk_general_transfer_desc;
+
+/* out = b - A x (b != NULL) or A x; out may alias b.  K1g. */
+int ivk_general_apply(const ivk_general_desc* op, const double* x, const double* b, double* out,
+                      void* stream);
+/* K7g: assemble every patch matrix R_i A R_i^T from the single-stage CSR
+ * (the stage-0 block of each patch's idx list is its sorted single-stage DoF
+ * list, the same for every stage) and invert it: full (s b)^2 inverses, or
+ * the Kronecker eigen-blocks when pd->kron is set (non-symmetric layout).
+ * Replaces _patch_matrices + np.linalg.inv (solvers.py:169-212). */
+int ivk_general_patch_factor(const ivk_general_desc* op, const ivk_patch_desc* pd,
+                             int32_t* singular_dev, void* stream);
+/* K1g -> K3 -> K4: x_out = x + omega W sum_i R_i^T A_i^-1 R_i (b - A x). */
+int ivk_general_vanka_sweep(const ivk_general_desc* op, const ivk_patch_desc* pd,
+                            const double* x, const double* b, double omega, const double* w,
+                            double* r, double* local, double* x_out, void* stream);
+/* out = 0 except out = src on constrained DoFs of every stage
+ * (MGHierarchyOp.precondition z[cd] = r[cd], solvers.py:352-354). */
+int ivk_general_seed_constrained(const ivk_general_desc* op, const double* src, double* out,
+                                 void* stream);
+/* rc = (I_s (x) P)^T rf with constrained coarse rows zeroed; xf += (I_s (x) P) ec
+ * on unconstrained fine rows (solvers.py:340-346). */
+int ivk_general_restrict(const ivk_general_transfer_desc* t, const double* rf, double* rc,
+                         void* stream);
+int ivk_general_prolong_add(const ivk_general_transfer_desc* t, const double* ec, double* xf,
+                            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

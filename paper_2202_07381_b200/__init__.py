@@ -12,6 +12,8 @@ from .mesh import Mesh2D, MeshHierarchy, build_hierarchy, crossed_grid, diagonal
 from .solvers import (CoarseSolver, KrylovStats, MGHierarchyOp, MGLevel, PatchSingularError,
                       SmootherSpec, VankaPatchSet, apply_vanka, build_vanka_patches,
                       chebyshev_smooth, coarse_direct_solve, fgmres, vcycle)
+from .general import GeneralStageSystem, GeneralTransfer
+from .mhd import MHDDiscretization, MHDParams
 from .stages import StageSystem, assemble_stage_operator
 from .tableaux import ButcherTableau, tableau_lookup
 

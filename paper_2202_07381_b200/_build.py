@@ -7,7 +7,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libivk.so")
-SOURCES = ["ivk_operator.cu", "ivk_patches.cu", "ivk_transfer.cu", "ivk_coarse.cu",
+SOURCES = ["ivk_operator.cu", "ivk_patches.cu", "ivk_transfer.cu", "ivk_coarse.cu", "ivk_general.cu",
            "ivk_krylov.cu", "ivk_assembly.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

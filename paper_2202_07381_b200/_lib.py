@@ -8,6 +8,7 @@ import ctypes as C
 import os
 
 __all__ = ["lib", "check", "OperatorDesc", "PatchDesc", "KronDesc", "TransferDesc", "CoarseDesc",
+           "GeneralDesc", "GeneralTransferDesc",
            "IVK_MAX_STAGES", "IvkError", "SingularPatch"]
 
 IVK_MAX_STAGES = 3
@@ -105,6 +106,25 @@ class CoarseDesc(C.Structure):
     ]
 
 
+class GeneralDesc(C.Structure):
+    _fields_ = [
+        ("stages", C.c_int32), ("n", C.c_int32), ("nnz", C.c_int32), ("dt", C.c_double),
+        ("butcher_a", C.c_double * (IVK_MAX_STAGES * IVK_MAX_STAGES)),
+        ("rowptr", C.c_void_p), ("col", C.c_void_p), ("ml", C.c_void_p),
+        ("sptr", C.c_void_p), ("scol", C.c_void_p), ("sml", C.c_void_p),
+        ("constrained", C.c_void_p),
+    ]
+
+
+class GeneralTransferDesc(C.Structure):
+    _fields_ = [
+        ("stages", C.c_int32), ("nf", C.c_int32), ("nc", C.c_int32),
+        ("p_rowptr", C.c_void_p), ("p_col", C.c_void_p), ("p_val", C.c_void_p),
+        ("pt_rowptr", C.c_void_p), ("pt_col", C.c_void_p), ("pt_val", C.c_void_p),
+        ("fine_constrained", C.c_void_p), ("coarse_constrained", C.c_void_p),
+    ]
+
+
 class QuadTable(C.Structure):
     _fields_ = [
         ("nq", C.c_int32),
@@ -156,6 +176,13 @@ _SIGS = {
     "ivk_mgs": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P, _P], C.c_int),
     "ivk_scale": ([C.c_int64, _P, _P, C.c_int32, _P, _P], C.c_int),
     "ivk_lincomb": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P], C.c_int),
+    "ivk_general_apply": ([C.POINTER(GeneralDesc), _P, _P, _P, _P], C.c_int),
+    "ivk_general_patch_factor": ([C.POINTER(GeneralDesc), C.POINTER(PatchDesc), _P, _P], C.c_int),
+    "ivk_general_vanka_sweep": ([C.POINTER(GeneralDesc), C.POINTER(PatchDesc), _P, _P, C.c_double,
+                                 _P, _P, _P, _P, _P], C.c_int),
+    "ivk_general_seed_constrained": ([C.POINTER(GeneralDesc), _P, _P, _P], C.c_int),
+    "ivk_general_restrict": ([C.POINTER(GeneralTransferDesc), _P, _P, _P], C.c_int),
+    "ivk_general_prolong_add": ([C.POINTER(GeneralTransferDesc), _P, _P, _P], C.c_int),
 }
 EXPORTED = tuple(_SIGS)
 

@@ -27,12 +27,9 @@ __device__ __forceinline__ double ld_stream(const double* p) {
   asm volatile("ld.global.L1::no_allocate.L2::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
-__device__ __forceinline__ double2 ld_stream2(const double2* p) {
-  double2 v;
-  asm volatile("ld.global.L1::no_allocate.L2::evict_first.v2.f64 {%0, %1}, [%2];"
-               : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-}
+// (the L2::evict_first qualifier needs a 256-bit vector on sm_100a; 128-bit
+// streams use the cache-streaming .cs hint instead)
+__device__ __forceinline__ double2 ld_stream2(const double2* p) { return __ldcs(p); }
 
 // ---- TMA bulk copies (cp.async.bulk global -> shared, mbarrier completion) --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

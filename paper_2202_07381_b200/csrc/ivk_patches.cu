@@ -18,7 +18,8 @@
 
 namespace ivk {
 
-int validate_op(const ivk_operator_desc* d);  // ivk_operator.cu
+int validate_op(const ivk_operator_desc* d);         // ivk_operator.cu
+int validate_general(const ivk_general_desc* d);     // ivk_general.cu
 
 struct PatchParams {
   int num_patches, dim, max_m, total_m;
@@ -778,6 +779,128 @@ __global__ void __launch_bounds__(kKronFactorThreads) patch_factor_kron_kernel(
   }
 }
 
+// ------------------------------------------------------- K7g (general path)
+//
+// One CTA per patch of a general stage operator I_s (x) M + dt A (x) L
+// (ivk_general_desc).  The stage-0 block of the patch's idx list is its
+// sorted single-stage DoF list (b = m / s entries, identical for every
+// stage); a warp per local row walks that row of the single-stage CSR and
+// binary-searches each column in the list, so the patch matrix R_i A R_i^T
+// is assembled straight into shared memory.  full: the (s b)^2 stage-coupled
+// matrix, Gauss-Jordan, Inv^T stored with ld = (m + 3) & ~3 (the K3 layout);
+// kron: one (complex) b x b block M^ + dt lam_k L^ per stored eigenvalue,
+// stored as G^T in the K3e layout.
+struct GenFactorParams {
+  int S;
+  double dt;
+  double a[IVK_MAX_STAGES * IVK_MAX_STAGES];
+  const int32_t* __restrict__ rowptr;
+  const int32_t* __restrict__ col;
+  const double2* __restrict__ ml;
+};
+
+constexpr int kGenFactorThreads = 256;
+constexpr int kGenMaxD = 512;
+
+__device__ __forceinline__ int find_sorted(const int* a, int n, int v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const int c = a[mid];
+    if (c == v) return mid;
+    if (c < v) lo = mid + 1; else hi = mid;
+  }
+  return -1;
+}
+
+__global__ void __launch_bounds__(kGenFactorThreads) general_factor_kernel(
+    GenFactorParams g, PatchParams pd, KronParams kp, int use_kron, int32_t* singular) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int piv[kGenMaxD];
+  __shared__ double colre[kGenMaxD], colim[kGenMaxD];
+  __shared__ int dofs[kGenMaxD];
+  __shared__ int s_prow, s_bad;
+  const int p = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  const int off = pd.idx_off[p], m = pd.idx_off[p + 1] - off, S = g.S, b = m / S;
+  for (int i = tid; i < b; i += blockDim.x) dofs[i] = pd.idx[off + i];
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  if (!use_kron) {
+    double* A = sm;
+    const int d = m;
+    for (int e = tid; e < d * d; e += blockDim.x) A[e] = 0.0;
+    __syncthreads();
+    for (int i = warp; i < b; i += nw) {
+      const int row = dofs[i];
+      for (int e = g.rowptr[row] + lane; e < g.rowptr[row + 1]; e += 32) {
+        const int j = find_sorted(dofs, b, g.col[e]);
+        if (j < 0) continue;
+        const double2 v = g.ml[e];
+        for (int x = 0; x < S; ++x)
+          for (int y = 0; y < S; ++y)
+            A[(long)(x * b + i) * d + y * b + j] = (x == y ? v.x : 0.0) + g.dt * g.a[x * S + y] * v.y;
+      }
+    }
+    __syncthreads();
+    if (!gauss_jordan<false>(A, nullptr, d, piv, colre, colim, &s_prow, &s_bad)) {
+      if (tid == 0) atomicMin(singular, pd.vertex[p]);
+      return;
+    }
+    const int ld = (d + 3) & ~3;
+    double* out = pd.inv + pd.inv_off[p];
+    for (int e = tid; e < d * ld; e += blockDim.x) {
+      const int j = e / ld, i = e - j * ld;
+      out[e] = (i < d) ? A[(long)i * d + j] : 0.0;
+    }
+    return;
+  }
+  double* Are = sm;
+  double* Aim = sm + b * b;
+  double* out = pd.inv + pd.inv_off[p];
+  for (int k = 0; k < kp.nblk; ++k) {
+    const bool cplx = kp.is_complex[k] != 0;
+    const double fre = g.dt * kp.lam_re[k], fim = g.dt * kp.lam_im[k];
+    for (int e = tid; e < b * b; e += blockDim.x) { Are[e] = 0.0; Aim[e] = 0.0; }
+    __syncthreads();
+    for (int i = warp; i < b; i += nw) {
+      const int row = dofs[i];
+      for (int e = g.rowptr[row] + lane; e < g.rowptr[row + 1]; e += 32) {
+        const int j = find_sorted(dofs, b, g.col[e]);
+        if (j < 0) continue;
+        const double2 v = g.ml[e];
+        Are[i * b + j] = v.x + fre * v.y;
+        Aim[i * b + j] = fim * v.y;
+      }
+    }
+    __syncthreads();
+    const bool ok = cplx ? gauss_jordan<true>(Are, Aim, b, piv, colre, colim, &s_prow, &s_bad)
+                         : gauss_jordan<false>(Are, Aim, b, piv, colre, colim, &s_prow, &s_bad);
+    if (!ok) {
+      if (tid == 0) atomicMin(singular, pd.vertex[p]);
+      return;
+    }
+    if (cplx) {
+      const int ldc = kron_ldc(b);
+      for (int e = tid; e < b * ldc; e += blockDim.x) {
+        const int j = e / ldc, i = e - j * ldc;
+        const bool in = i < b;
+        out[2 * e] = in ? Are[i * b + j] : 0.0;
+        out[2 * e + 1] = in ? Aim[i * b + j] : 0.0;
+      }
+      out += 2 * b * ldc;
+    } else {
+      const int ldr = kron_ldr(b);
+      for (int e = tid; e < b * ldr; e += blockDim.x) {
+        const int j = e / ldr, i = e - j * ldr;
+        out[e] = (i < b) ? Are[i * b + j] : 0.0;
+      }
+      out += b * ldr;
+    }
+    __syncthreads();
+  }
+}
+
 // Warp per patch.  Gather r_p, transform to the eigenbasis, one streamed
 // GEMV per stored block (lanes split into G groups of CPC lanes; each lane
 // owns a 32-byte row chunk, groups take interleaved columns), back-transform.
@@ -910,6 +1033,142 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_kernel(
       double acc = 0.0;
       for (int k = 0; k < kp.nblk; ++k) {
         const double zr = rt_all[warp][k][2 * a], zi = rt_all[warp][k][2 * a + 1];
+        acc += kp.scale[k] * (kp.v_re[i * S + k] * zr - kp.v_im[i * S + k] * zi);
+      }
+      st_keep(local + (pd.slot_pos ? pd.slot_pos[off + e] : off + e), acc);
+    }
+    __syncwarp();
+  }
+}
+
+// Blocks up to b = 128 (general path, MHD: b = 78): the same algorithm with
+// per-warp buffers in dynamic shared memory; complex blocks wider than 64
+// rows (more than 32 chunks per column) take a multi-pass column walk.
+// Dynamic shared memory: per warp S*bmax (r_p) + nblk*2*bmax (eigenbasis
+// vectors) + 2*bmax + 128 (partials) doubles.
+__host__ __device__ __forceinline__ int kron_apply_seg(int S, int nblk, int bmax) {
+  return S * bmax + nblk * 2 * bmax + 128 + 2 * bmax + 8;
+}
+
+__global__ void __launch_bounds__(kApplyWarps * 32, 4) patch_apply_kron_wide_kernel(
+    PatchParams pd, KronParams kp, const double* __restrict__ r, double* __restrict__ local,
+    int bmax) {
+  extern __shared__ __align__(16) double kron_sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = kp.S;
+  double* rs = kron_sm + (long)warp * kron_apply_seg(S, kp.nblk, bmax);
+  double* rtb = rs + S * bmax;                 // block k: rtb + k * 2 * bmax
+  double* red = rtb + kp.nblk * 2 * bmax;      // 128 partials
+  double* zt = red + 128;                      // block result, chunk layout
+  const int stride = gridDim.x * kApplyWarps;
+  for (int p = blockIdx.x * kApplyWarps + warp; p < pd.num_patches; p += stride) {
+    const int off = pd.idx_off[p];
+    const int m = pd.idx_off[p + 1] - off;
+    const int b = m / S;
+    for (int j = lane; j < m; j += 32) rs[j] = __ldg(r + pd.idx[off + j]);
+    __syncwarp();
+    // r~_k[a] = sum_i Vinv[k][i] r[i][a]
+    for (int e = lane; e < kp.nblk * b; e += 32) {
+      const int k = e / b, a = e - k * b;
+      double re = 0.0, im = 0.0;
+      for (int i = 0; i < S; ++i) {
+        const double x = rs[i * b + a];
+        re = fma(kp.vinv_re[k * S + i], x, re);
+        im = fma(kp.vinv_im[k * S + i], x, im);
+      }
+      rtb[k * 2 * bmax + 2 * a] = re;
+      rtb[k * 2 * bmax + 2 * a + 1] = im;
+    }
+    __syncwarp();
+    const double* G = pd.inv + pd.inv_off[p];
+    for (int k = 0; k < kp.nblk; ++k) {
+      double* rt = rtb + k * 2 * bmax;
+      const bool cplx = kp.is_complex[k] != 0;
+      const int ldd = cplx ? 2 * kron_ldc(b) : kron_ldr(b);  // doubles per column
+      const int cpc = ldd >> 2;                               // 32-byte chunks per column
+      // passes of <= 32 chunks; inside a pass the lanes split into
+      // groups = 32 / cc groups of cc lanes (one 32-byte row chunk each) that
+      // take interleaved columns, so a 39-chunk complex column (b = 78) runs
+      // as 32 chunks x 1 group, then 7 chunks x 4 groups
+      for (int c0 = 0; c0 < cpc; c0 += 32) {
+        const int cc = min(32, cpc - c0);
+        const int groups = 32 / cc;
+        const int g = lane / cc, c = c0 + lane - g * cc;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (g < groups) {
+          const double* col = G + 4 * c;
+          int j = g;
+          for (; j + 3 * groups < b; j += 4 * groups) {
+            double v[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              ld_stream4(col + (long)(j + u * groups) * ldd, v[u][0], v[u][1], v[u][2], v[u][3]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double xr = rt[2 * (j + u * groups)], xi = rt[2 * (j + u * groups) + 1];
+              if (cplx) {
+                a0 = fma(v[u][0], xr, fma(-v[u][1], xi, a0));
+                a1 = fma(v[u][0], xi, fma(v[u][1], xr, a1));
+                a2 = fma(v[u][2], xr, fma(-v[u][3], xi, a2));
+                a3 = fma(v[u][2], xi, fma(v[u][3], xr, a3));
+              } else {
+                a0 = fma(v[u][0], xr, a0);
+                a1 = fma(v[u][1], xr, a1);
+                a2 = fma(v[u][2], xr, a2);
+                a3 = fma(v[u][3], xr, a3);
+              }
+            }
+          }
+          for (; j < b; j += groups) {
+            double v0, v1, v2, v3;
+            ld_stream4(col + (long)j * ldd, v0, v1, v2, v3);
+            const double xr = rt[2 * j], xi = rt[2 * j + 1];
+            if (cplx) {
+              a0 = fma(v0, xr, fma(-v1, xi, a0));
+              a1 = fma(v0, xi, fma(v1, xr, a1));
+              a2 = fma(v2, xr, fma(-v3, xi, a2));
+              a3 = fma(v2, xi, fma(v3, xr, a3));
+            } else {
+              a0 = fma(v0, xr, a0);
+              a1 = fma(v1, xr, a1);
+              a2 = fma(v2, xr, a2);
+              a3 = fma(v3, xr, a3);
+            }
+          }
+        }
+        red[4 * lane + 0] = a0;
+        red[4 * lane + 1] = a1;
+        red[4 * lane + 2] = a2;
+        red[4 * lane + 3] = a3;
+        __syncwarp();
+        // fixed-order sum over the groups -> zt[4 c .. 4 c + 3]
+        for (int e = lane; e < 4 * cc; e += 32) {
+          const int ch = e >> 2, q = e & 3;
+          double acc = 0.0;
+          for (int gg = 0; gg < groups; ++gg) acc += red[4 * (gg * cc + ch) + q];
+          zt[4 * (c0 + ch) + q] = acc;
+        }
+        __syncwarp();
+      }
+      // z~_k: complex chunks hold (re, im) interleaved rows, real chunks 4 rows
+      for (int a = lane; a < b; a += 32) {
+        if (cplx) {
+          rt[2 * a] = zt[2 * a];
+          rt[2 * a + 1] = zt[2 * a + 1];
+        } else {
+          rt[2 * a] = zt[a];
+          rt[2 * a + 1] = 0.0;
+        }
+      }
+      G += cplx ? 2L * b * kron_ldc(b) : (long)b * kron_ldr(b);
+      __syncwarp();
+    }
+    // z[i][a] = sum_k scale_k Re(V[i][k] z~_k[a])
+    for (int e = lane; e < m; e += 32) {
+      const int i = e / b, a = e - i * b;
+      double acc = 0.0;
+      for (int k = 0; k < kp.nblk; ++k) {
+        const double zr = rtb[k * 2 * bmax + 2 * a], zi = rtb[k * 2 * bmax + 2 * a + 1];
         acc += kp.scale[k] * (kp.v_re[i * S + k] * zr - kp.v_im[i * S + k] * zi);
       }
       st_keep(local + (pd.slot_pos ? pd.slot_pos[off + e] : off + e), acc);
@@ -1385,8 +1644,22 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       fn<<<cgrid, kClassWarps * 32, smem, st>>>(p, dd, kp, r, local, g);
     } else if (bmax <= 64)
       patch_apply_kron_kernel<64><<<grid, kApplyWarps * 32, 0, st>>>(p, kp, r, local);
-    else {
-      set_error("ivk_patch_apply: kron block size %d > 64 unsupported", bmax);
+    else if (bmax <= 128) {
+      const size_t smem =
+          (size_t)kApplyWarps * kron_apply_seg(S, k->nblk, bmax) * sizeof(double);
+      void (*fn)(PatchParams, KronParams, const double*, double*, int) =
+          patch_apply_kron_wide_kernel;
+      if (smem > 48 * 1024) {
+        cudaError_t e =
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) {
+          set_error("ivk_patch_apply: %s", cudaGetErrorString(e));
+          return IVK_ECUDA;
+        }
+      }
+      fn<<<grid, kApplyWarps * 32, smem, st>>>(p, kp, r, local, bmax);
+    } else {
+      set_error("ivk_patch_apply: kron block size %d > 128 unsupported", bmax);
       return IVK_EUNSUPPORTED;
     }
     return check_launch("ivk_patch_apply(kron)");
@@ -1496,6 +1769,64 @@ int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int3
   patch_factor_kernel<<<pd->num_patches, kFactorThreads, smem, as_stream(stream)>>>(f, p,
                                                                                     singular_dev);
   return check_launch("ivk_patch_factor");
+}
+
+int ivk_general_patch_factor(const ivk_general_desc* op, const ivk_patch_desc* pd,
+                             int32_t* singular_dev, void* stream) {
+  int rc = validate_general(op);
+  if (rc) return rc;
+  rc = validate_patches(pd);
+  if (rc) return rc;
+  IVK_REQUIRE(pd->vertex && singular_dev, "patch factorisation needs vertex ids and a singular flag");
+  const int S = op->stages;
+  IVK_REQUIRE(pd->max_m <= kGenMaxD, "patch size %d > %d unsupported", pd->max_m, kGenMaxD);
+  GenFactorParams g;
+  g.S = S;
+  g.dt = op->dt;
+  for (int i = 0; i < IVK_MAX_STAGES * IVK_MAX_STAGES; ++i) g.a[i] = op->butcher_a[i];
+  g.rowptr = op->rowptr;
+  g.col = op->col;
+  g.ml = reinterpret_cast<const double2*>(op->ml);
+  KronParams kp{};
+  size_t smem;
+  const int use_kron = pd->kron != nullptr;
+  if (use_kron) {
+    const ivk_kron_desc* k = pd->kron;
+    IVK_REQUIRE(!k->symmetric, "the general path stores non-symmetric eigen-blocks");
+    int SS = 0;
+    for (int i = 0; i < k->nblk; ++i) SS += k->is_complex[i] ? 2 : 1;
+    IVK_REQUIRE(SS == S, "kron blocks do not cover %d stages", S);
+    kp = make_kron(k, S);
+    const int bmax = pd->max_m / S;
+    smem = 2 * (size_t)bmax * bmax * sizeof(double);
+  } else {
+    smem = (size_t)pd->max_m * pd->max_m * sizeof(double);
+  }
+  if (smem > 200 * 1024) {
+    set_error("ivk_general_patch_factor: patch (m = %d) exceeds shared memory", pd->max_m);
+    return IVK_EUNSUPPORTED;
+  }
+  cudaError_t e = cudaFuncSetAttribute(general_factor_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) {
+    set_error("ivk_general_patch_factor: %s", cudaGetErrorString(e));
+    return IVK_ECUDA;
+  }
+  PatchParams p = make_patch_params(pd);
+  general_factor_kernel<<<pd->num_patches, kGenFactorThreads, smem, as_stream(stream)>>>(
+      g, p, kp, use_kron, singular_dev);
+  return check_launch("ivk_general_patch_factor");
+}
+
+int ivk_general_vanka_sweep(const ivk_general_desc* op, const ivk_patch_desc* pd, const double* x,
+                            const double* b, double omega, const double* w, double* r,
+                            double* local, double* x_out, void* stream) {
+  IVK_REQUIRE(x && b && r && local && x_out, "sweep vector is NULL");
+  int rc = ivk_general_apply(op, x, b, r, stream);
+  if (rc) return rc;
+  rc = ivk_patch_apply(pd, r, local, stream);
+  if (rc) return rc;
+  return ivk_patch_combine(pd, local, x, 1.0, omega, w, x_out, nullptr, stream);
 }
 
 int ivk_vanka_sweep(const ivk_operator_desc* op, const ivk_patch_desc* pd, const double* x,

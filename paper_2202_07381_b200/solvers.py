@@ -230,9 +230,15 @@ class VankaPatchSet:
         self.system = system
         # vertices: only the patches of these centre vertices (one shard of a
         # partitioned level, shard.py); None = every vertex
-        self.tables = build_patch_tables(mesh, system.n_nodes, system.n_p, system.r,
-                                         system.node_constrained, vertices=vertices,
-                                         ncomp=system.nc)
+        # general multi-field systems (general.py, e.g. MHD) build their own
+        # vertex-star tables; Taylor-Hood systems use the reference layout
+        self.general = getattr(system, "general", False)
+        if self.general:
+            self.tables = system.patch_tables(mesh, vertices=vertices)
+        else:
+            self.tables = build_patch_tables(mesh, system.n_nodes, system.n_p, system.r,
+                                             system.node_constrained, vertices=vertices,
+                                             ncomp=system.nc)
         self.num_patches = self.tables.num_patches
         if mode not in ("auto", "full", "kron", "kron-sym", "dedup"):
             raise ValueError(f"unknown patch mode {mode!r}")
@@ -245,12 +251,17 @@ class VankaPatchSet:
         self.dedup = None
         if mode == "dedup" and system.convection is not None:
             raise ValueError("dedup needs a translation-invariant (convection-free) operator")
+        if self.general and mode in ("kron-sym", "dedup"):
+            raise ValueError(f"mode {mode!r} is not available for general operators")
         if mode in ("auto", "kron", "kron-sym", "dedup"):
             try:
                 shared = system.convection is None or len(system._conv_vals) == 1
                 if not shared:
                     raise ValueError("per-stage convection Jacobians differ")
-                if self.tables.max_m // system.r > 64:
+                # K7e (Stokes) holds 2 b^2 doubles in shared memory up to b = 64;
+                # K7g (general) up to 200 KB; K3e streams blocks up to b = 128
+                bmax = self.tables.max_m // system.r
+                if bmax > (112 if self.general else 64):
                     raise ValueError("patch block too large for the kron kernels")
                 # Stokes (no convection): S^ symmetric -> packed symmetric blocks
                 self.kron = KronSplit(system.tableau.A,
@@ -259,8 +270,9 @@ class VankaPatchSet:
                 if mode in ("kron", "kron-sym", "dedup"):
                     raise
                 self.kron = None
-        if self.kron is not None and (mode == "dedup" or (mode == "auto" and system.nc == 2 and
-                                                           system.convection is None)):
+        if self.kron is not None and not self.general and (
+                mode == "dedup" or (mode == "auto" and system.nc == 2 and
+                                    system.convection is None)):
             # translation-invariant operator: share inverses between patches
             # whose canonical matrices are bitwise identical (dedup.py); "auto"
             # keeps it only when it actually collapses the patch set
@@ -469,8 +481,11 @@ class VankaPatchSet:
         dev = self.device_data()
         flag = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev["idx"].device)
         target = dev["rep_desc"] if self.dedup is not None else dev["desc"]
-        _lib.check(_lib.lib().ivk_patch_factor(self.system.desc, target, ptr(flag), stream()),
-                   "patch_factor")
+        if self.general:
+            self.system.factor_patches(target, flag)
+        else:
+            _lib.check(_lib.lib().ivk_patch_factor(self.system.desc, target, ptr(flag), stream()),
+                       "patch_factor")
         bad = int(flag.item())
         if bad != 2 ** 31 - 1:
             raise PatchSingularError(bad)
@@ -581,6 +596,9 @@ def apply_vanka(patches, system, x, b, omega=None, weights=None, workspace=None,
         r, local = torch.empty_like(xd), dev["local"]
     if out is None:
         out = torch.empty_like(xd)
+    if getattr(system, "general", False):
+        system.vanka_sweep(dev["desc"], xd, bd, w, wd, r, local, out)
+        return to_host(out) if host else out
     _lib.check(_lib.lib().ivk_vanka_sweep(system.desc, dev["desc"], ptr(xd), ptr(bd), float(w),
                                           ptr(wd), ptr(r), ptr(local), ptr(out), stream()),
                "vanka_sweep")
@@ -921,6 +939,11 @@ class MGHierarchyOp:
         from ._device import ptr, stream
         sys_ = self.finest
         dev = sys_.device_data()
+        if getattr(sys_, "general", False):
+            sys_.seed_constrained_into(r, z)
+            self._cycle(len(self.levels) - 1, z, r)
+            sys_.project_pressure_means(z)
+            return z
         _lib.check(_lib.lib().ivk_seed_constrained(sys_.r, sys_.n_nodes, sys_.nc, sys_.n_p,
                                                    ptr(dev["tensors"]["cmask"]), ptr(r), ptr(z),
                                                    stream()), "seed_constrained")

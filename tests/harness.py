@@ -82,3 +82,48 @@ def load_golden(name):
     with open(os.path.join(GOLDEN, f"{name}.json")) as fh:
         meta = json.load(fh)
     return data, meta
+
+
+# BASELINE config 5 (2-D resistive MHD, mhd.py) and reduced parity cases with
+# its scheme.  No reference implementation exists: parity is against the
+# oracle restatement only (oracle/general_oracle.py, "parity unpinned").
+MHD_CONFIGS = {
+    "cfg5": dict(n0=8, level=4, Re=100.0, Rm=100.0, S=1.0, family="radauiia", stages=2,
+                 dt=1 / 128, seed=4),
+    "mhd16": dict(n0=8, level=1, Re=100.0, Rm=100.0, S=1.0, family="radauiia", stages=2,
+                  dt=1 / 128, seed=4),
+    "mhd32": dict(n0=8, level=2, Re=100.0, Rm=100.0, S=1.0, family="radauiia", stages=2,
+                  dt=1 / 128, seed=4),
+    "mhd16s3": dict(n0=8, level=1, Re=100.0, Rm=100.0, S=1.0, family="radauiia", stages=3,
+                    dt=1 / 128, seed=5),
+}
+
+
+def mhd_setup(name):
+    from paper_2202_07381_b200.mhd import MHDDiscretization, MHDParams
+    case = MHD_CONFIGS[name]
+    disc = MHDDiscretization(case["n0"], case["level"],
+                             MHDParams(case["Re"], case["Rm"], case["S"]))
+    return disc, tableau_lookup(case["family"], case["stages"]), case
+
+
+def mhd_oracle_levels(disc, tab, dt, levels=None, patches=True):
+    """Oracle operators / patches / stage prolongations on every MHD level."""
+    import scipy.sparse as sp
+    from oracle.general_oracle import (OracleGeneralOperator, OracleGeneralPatches,
+                                       oracle_general_patch_indices)
+    out = []
+    ks = range(disc.num_levels) if levels is None else levels
+    for k in ks:
+        o = disc.ops[k]
+        n_nodes, nv, n1 = o["layout"]
+        M = sp.csr_matrix((o["m"], o["col"], o["rowptr"]), shape=(n1, n1))
+        L = sp.csr_matrix((o["l"], o["col"], o["rowptr"]), shape=(n1, n1))
+        op = OracleGeneralOperator(M, L, tab.A, dt, np.flatnonzero(o["cmask"]), n1 - nv)
+        mesh = disc.hier.levels[k]
+        idxs = oracle_general_patch_indices(mesh.cells, mesh.cell_to_edges, mesh.num_vertices,
+                                            op, 4, 2)
+        pat = OracleGeneralPatches(op, idxs) if (k > 0 and patches) else None
+        P = disc.stage_prolong(k, tab.r).matrix if k > 0 else None
+        out.append({"op": op, "patches": pat, "prolong": P, "idxs": idxs})
+    return out

@@ -45,6 +45,8 @@ STRUCTS = {
     "ivk_coarse_desc": _lib.CoarseDesc,
     "ivk_quad_table": _lib.QuadTable,
     "ivk_convection_desc": _lib.ConvectionDesc,
+    "ivk_general_desc": _lib.GeneralDesc,
+    "ivk_general_transfer_desc": _lib.GeneralTransferDesc,
 }
 
 
