@@ -360,10 +360,8 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     # the headline sweep runs the general per-patch formulation (kron: every
-    # patch streams its own eigen-split inverse blocks from HBM; 3-D patches
-    # (b ~ 196) take the full per-patch inverse)
-    mg, S = disc.build_mg(tab, cfg["dt"], cheb, convection=conv,
-                          patch_mode="auto" if is3d else "kron")
+    # patch streams its own eigen-split inverse blocks from HBM)
+    mg, S = disc.build_mg(tab, cfg["dt"], cheb, convection=conv, patch_mode="kron")
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     pou = SmootherSpec(pre=2, post=2, accel="richardson", omega=om, weighting="pou")
@@ -499,8 +497,8 @@ def run_ours(args, rank, world, local):
                                 "inverse_bytes": 8 * fine.inv_size}}
     if not args.no_full_mode:
         from paper_2202_07381_b200 import VankaPatchSet
-        others = [] if is3d else (["full"] if (is_mhd or conv is not None)
-                                  else ["dedup", "kron-sym", "full"])
+        others = ["full"] if (is3d or is_mhd or conv is not None) \
+            else ["dedup", "kron-sym", "full"]
         for other in others:
             if other == fine.mode:
                 continue

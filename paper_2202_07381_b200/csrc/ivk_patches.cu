@@ -779,6 +779,170 @@ __global__ void __launch_bounds__(kKronFactorThreads) patch_factor_kron_kernel(
   }
 }
 
+// Kronecker eigen-blocks too large for shared memory (3-D: b = 3k + 1 ~ 176):
+// persistent CTAs, each block assembled TRANSPOSED straight into its own
+// slot of the inverse store -- complex blocks as interleaved (re, im) with
+// leading dimension ldc, real blocks with ldr -- and inverted in place by
+// Gauss-Jordan with row pivoting: (A^T)^-1 = (A^-1)^T = G^T, exactly the K3e
+// layout, so no scratch and no final transpose (cf. patch_factor_global_kernel).
+template <int NC>
+__global__ void __launch_bounds__(kFactorGlobalThreads) patch_factor_kron_global_kernel(
+    FactorParams op, PatchParams pd, KronParams kp, int32_t* singular) {
+  __shared__ double prow[2 * 512];
+  __shared__ double colk[2 * 512];
+  __shared__ int piv[512];
+  __shared__ int s_prow, s_bad;
+  const int tid = threadIdx.x;
+  for (int p = blockIdx.x; p < pd.num_patches; p += gridDim.x) {
+    const int n0 = pd.node_off[p], nk = pd.node_off[p + 1] - n0;
+    const int* nodes = pd.node + n0;
+    const int v = pd.vertex[p];
+    const int mv = NC * nk, b = mv + 1;
+    double* out = pd.inv + pd.inv_off[p];
+    bool bad = false;
+    for (int k = 0; k < kp.nblk && !bad; ++k) {
+      const bool cplx = kp.is_complex[k] != 0;
+      const double fre = op.dt * kp.lam_re[k], fim = op.dt * kp.lam_im[k];
+      const int ld = cplx ? kron_ldc(b) : kron_ldr(b);
+      const int w = cplx ? 2 : 1;  // doubles per element
+      double* B = out;             // B[(c * ld + r) * w] = A[r][c]
+      for (int e = tid; e < b * ld * w; e += blockDim.x) B[e] = 0.0;
+      if (tid == 0) s_bad = 0;
+      __syncthreads();
+      for (int pr = tid; pr < nk * nk; pr += blockDim.x) {
+        const int al = pr / nk, be = pr % nk;
+        const int row = nodes[al];
+        const int pos = find_col(op.p2_col, op.p2_rowptr[row], op.p2_rowptr[row + 1], nodes[be]);
+        if (pos < 0) continue;
+        const double2 mk = op.p2_mk[pos];
+        for (int cc = 0; cc < NC; ++cc) {
+          const long e = (long)(NC * be + cc) * ld + NC * al + cc;  // A[NC al + cc][NC be + cc]
+          B[e * w] = mk.x + fre * mk.y;
+          if (cplx) B[e * w + 1] = fim * mk.y;
+        }
+      }
+      for (int al = tid; al < nk; al += blockDim.x) {
+        const int row = nodes[al];
+        const int pos = find_col(op.b_col, op.b_rowptr[row], op.b_rowptr[row + 1], v);
+        for (int cc = 0; cc < NC; ++cc) {
+          const double bv = pos >= 0 ? op.b_raw[(long)pos * NC + cc] : 0.0;
+          const long e1 = (long)mv * ld + NC * al + cc;      // A[NC al + cc][mv]
+          const long e2 = (long)(NC * al + cc) * ld + mv;    // A[mv][NC al + cc]
+          B[e1 * w] = fre * bv;
+          B[e2 * w] = fre * bv;
+          if (cplx) {
+            B[e1 * w + 1] = fim * bv;
+            B[e2 * w + 1] = fim * bv;
+          }
+        }
+      }
+      __syncthreads();
+      for (int kk = 0; kk < b; ++kk) {
+        if (tid < 32) {
+          double best = -1.0;
+          int bi = kk;
+          for (int i = kk + tid; i < b; i += 32) {
+            const long e = ((long)i * ld + kk) * w;
+            double a = fabs(B[e]);
+            if (cplx) a += fabs(B[e + 1]);
+            if (a > best) { best = a; bi = i; }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_down_sync(0xffffffffu, best, o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+          }
+          if (tid == 0) {
+            s_prow = bi;
+            piv[kk] = bi;
+            if (!(best > 0.0)) s_bad = 1;
+          }
+        }
+        __syncthreads();
+        if (s_bad) break;
+        const int pr = s_prow;
+        const long pe = ((long)pr * ld + kk) * w;
+        double ir, ii = 0.0;
+        if (cplx) {
+          const double xr = B[pe], xi = B[pe + 1], den = xr * xr + xi * xi;
+          ir = xr / den;
+          ii = -xi / den;
+        } else {
+          ir = 1.0 / B[pe];
+        }
+        // scaled pivot row (swapped in) and the multiplier column
+        for (int j = tid; j < b; j += blockDim.x) {
+          const long e = ((long)pr * ld + j) * w;
+          if (j == kk) {
+            prow[w * j] = ir;
+            if (cplx) prow[w * j + 1] = ii;
+          } else if (cplx) {
+            const double xr = B[e], xi = B[e + 1];
+            prow[2 * j] = xr * ir - xi * ii;
+            prow[2 * j + 1] = xr * ii + xi * ir;
+          } else {
+            prow[j] = B[e] * ir;
+          }
+        }
+        for (int i = tid; i < b; i += blockDim.x) {
+          const long e = ((long)(i == pr ? kk : i) * ld + kk) * w;
+          colk[w * i] = B[e];
+          if (cplx) colk[w * i + 1] = B[e + 1];
+        }
+        __syncthreads();
+        if (pr != kk)
+          for (int j = tid; j < b * w; j += blockDim.x)
+            B[(long)pr * ld * w + j] = B[(long)kk * ld * w + j];
+        __syncthreads();
+        {
+          const int wp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+          for (int i = wp; i < b; i += nw) {
+            double* arow = B + (long)i * ld * w;
+            if (i == kk) {
+              for (int j = lane; j < b * w; j += 32) arow[j] = prow[j];
+            } else if (cplx) {
+              const double fr = colk[2 * i], fi = colk[2 * i + 1];
+              for (int j = lane; j < b; j += 32) {
+                const double br = (j == kk) ? 0.0 : arow[2 * j];
+                const double bi = (j == kk) ? 0.0 : arow[2 * j + 1];
+                const double pr2 = prow[2 * j], pi2 = prow[2 * j + 1];
+                arow[2 * j] = br - (fr * pr2 - fi * pi2);
+                arow[2 * j + 1] = bi - (fr * pi2 + fi * pr2);
+              }
+            } else {
+              const double f = colk[i];
+              for (int j = lane; j < b; j += 32) {
+                const double base = (j == kk) ? 0.0 : arow[j];
+                arow[j] = base - f * prow[j];
+              }
+            }
+          }
+        }
+        __syncthreads();
+      }
+      if (s_bad) {
+        if (tid == 0) atomicMin(singular, v);
+        bad = true;
+        __syncthreads();
+        break;
+      }
+      for (int kk = b - 1; kk >= 0; --kk) {
+        const int pk = piv[kk];
+        if (pk != kk) {
+          for (int i = tid; i < b; i += blockDim.x) {
+            const long e1 = ((long)i * ld + kk) * w, e2 = ((long)i * ld + pk) * w;
+            double t = B[e1]; B[e1] = B[e2]; B[e2] = t;
+            if (cplx) { t = B[e1 + 1]; B[e1 + 1] = B[e2 + 1]; B[e2 + 1] = t; }
+          }
+        }
+        __syncthreads();
+      }
+      out += (long)b * ld * w;
+    }
+  }
+}
+
 // ------------------------------------------------------- K7g (general path)
 //
 // One CTA per patch of a general stage operator I_s (x) M + dt A (x) L
@@ -1041,7 +1205,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_kernel(
   }
 }
 
-// Blocks up to b = 128 (general path, MHD: b = 78): the same algorithm with
+// Blocks up to b = 256 (MHD: b = 78, 3-D Stokes: b = 176): the same algorithm with
 // per-warp buffers in dynamic shared memory; complex blocks wider than 64
 // rows (more than 32 chunks per column) take a multi-pass column walk.
 // Dynamic shared memory: per warp S*bmax (r_p) + nblk*2*bmax (eigenbasis
@@ -1644,7 +1808,7 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       fn<<<cgrid, kClassWarps * 32, smem, st>>>(p, dd, kp, r, local, g);
     } else if (bmax <= 64)
       patch_apply_kron_kernel<64><<<grid, kApplyWarps * 32, 0, st>>>(p, kp, r, local);
-    else if (bmax <= 128) {
+    else if (bmax <= 256) {
       const size_t smem =
           (size_t)kApplyWarps * kron_apply_seg(S, k->nblk, bmax) * sizeof(double);
       void (*fn)(PatchParams, KronParams, const double*, double*, int) =
@@ -1659,7 +1823,7 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       }
       fn<<<grid, kApplyWarps * 32, smem, st>>>(p, kp, r, local, bmax);
     } else {
-      set_error("ivk_patch_apply: kron block size %d > 128 unsupported", bmax);
+      set_error("ivk_patch_apply: kron block size %d > 256 unsupported", bmax);
       return IVK_EUNSUPPORTED;
     }
     return check_launch("ivk_patch_apply(kron)");
@@ -1720,7 +1884,22 @@ int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int3
     IVK_REQUIRE(S == op->stages, "kron blocks do not cover %d stages", op->stages);
     IVK_REQUIRE(op->n_conv <= 1, "kron split needs one convection Jacobian shared by all stages");
     const int bmax = pd->max_m / S;
-    IVK_REQUIRE(bmax <= 64, "kron block size %d > 64 unsupported", bmax);
+    IVK_REQUIRE(bmax <= 256, "kron block size %d > 256 unsupported", bmax);
+    if (bmax > 64 || op->ncomp == 3) {
+      IVK_REQUIRE(!k->symmetric, "large kron blocks are stored non-symmetric");
+      IVK_REQUIRE(op->n_conv == 0, "large-patch factorisation supports no convection");
+      FactorParams f = make_factor_params(op);
+      PatchParams p = make_patch_params(pd);
+      KronParams kp = make_kron(k, S);
+      int grid = pd->num_patches < 2 * kSMs ? pd->num_patches : 2 * kSMs;
+      if (f.ncomp == 3)
+        patch_factor_kron_global_kernel<3><<<grid, kFactorGlobalThreads, 0, as_stream(stream)>>>(
+            f, p, kp, singular_dev);
+      else
+        patch_factor_kron_global_kernel<2><<<grid, kFactorGlobalThreads, 0, as_stream(stream)>>>(
+            f, p, kp, singular_dev);
+      return check_launch("ivk_patch_factor(kron, global)");
+    }
     const size_t smem = 2 * (size_t)bmax * bmax * sizeof(double);
     static size_t configured = 0;
     if (smem > configured) {

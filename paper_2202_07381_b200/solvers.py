@@ -258,10 +258,13 @@ class VankaPatchSet:
                 shared = system.convection is None or len(system._conv_vals) == 1
                 if not shared:
                     raise ValueError("per-stage convection Jacobians differ")
-                # K7e (Stokes) holds 2 b^2 doubles in shared memory up to b = 64;
-                # K7g (general) up to 200 KB; K3e streams blocks up to b = 128
+                # K7e (Stokes) factors b <= 64 in shared memory and larger
+                # blocks (3-D) in place in global memory up to b = 256; K7g
+                # (general) holds 2 b^2 doubles in shared memory (b <= 112);
+                # K3e streams blocks up to b = 256.  kron-sym / dedup: b <= 64
                 bmax = self.tables.max_m // system.r
-                if bmax > (112 if self.general else 64):
+                if bmax > (112 if self.general else 256) or \
+                        (mode in ("kron-sym", "dedup") and bmax > 64):
                     raise ValueError("patch block too large for the kron kernels")
                 # Stokes (no convection): S^ symmetric -> packed symmetric blocks
                 self.kron = KronSplit(system.tableau.A,

@@ -1,6 +1,8 @@
 """3-D Stokes on Kuhn tetrahedra (BASELINE config 4 family) through the C
 ABI: K1 with three components per node, the large-patch K7 (global-memory
-Gauss-Jordan on the transposed patch matrix), K3 full, K5 with ncomp = 3,
+Gauss-Jordan on the transposed patch matrix, full (s b)^2 inverses or the
+Kronecker eigen-blocks, b = 3k + 1 ~ 100-200), K3 full and the wide-block
+K3e, K5 with ncomp = 3,
 against the CPU oracle on the same host setup.  The reference has no 3-D
 discretisation: parity is to this repo's oracle restatement."""
 
@@ -16,8 +18,8 @@ pytestmark = pytest.mark.gpu
 _cache = {}
 
 
-def _case(family="radauiia", stages=2):
-    key = (family, stages)
+def _case(family="radauiia", stages=2, mode="kron"):
+    key = (family, stages, mode)
     if key in _cache:
         return _cache[key]
     from paper_2202_07381_b200 import SmootherSpec, tableau_lookup
@@ -26,7 +28,7 @@ def _case(family="radauiia", stages=2):
     tab = tableau_lookup(family, stages)
     dt = 1 / 32
     cheb = SmootherSpec(pre=2, post=2, accel="chebyshev", cheby_a=2.0, cheby_b=8.0)
-    mg, S = disc.build_mg(tab, dt, cheb)
+    mg, S = disc.build_mg(tab, dt, cheb, patch_mode=mode)
     lv = []
     for k in range(disc.num_levels):
         blk, mesh = disc.blocks[k], disc.hier.levels[k]
@@ -39,23 +41,38 @@ def _case(family="radauiia", stages=2):
     return _cache[key]
 
 
-def test_three_stage_3d_patches_unsupported():
-    """s = 3 gives 3-D patches of 588 unknowns: past the 512-row K3/K7 kernels,
-    rejected loudly (no fallback)."""
+def test_three_stage_3d_full_patches_unsupported():
+    """s = 3 gives 3-D patches of 588 unknowns: past the 512-row full K3/K7
+    kernels, rejected loudly (no fallback); the eigen-split (b = 196) runs."""
     from paper_2202_07381_b200 import SmootherSpec, tableau_lookup
     from paper_2202_07381_b200._lib import IvkError
     from paper_2202_07381_b200.fem3d import Discretization3D
     disc = Discretization3D(2, 1)
     with pytest.raises(IvkError):
-        disc.build_mg(tableau_lookup("radauiia", 3), 1 / 32, SmootherSpec())
+        disc.build_mg(tableau_lookup("radauiia", 3), 1 / 32, SmootherSpec(), patch_mode="full")
 
 
-@pytest.mark.parametrize("fam", [("radauiia", 2), ("gauss", 2), ("lobattoiiic", 2)])
-def test_matvec_and_sweep_3d(fam):
-    disc, tab, dt, mg, S, lv = _case(*fam)
+def test_three_stage_3d_kron():
+    from paper_2202_07381_b200 import apply_vanka
+    disc, tab, dt, mg, S, lv = _case("radauiia", 3, "kron")
     op, pat = lv[-1]["op"], lv[-1]["patches"]
     fine = mg.levels[-1].patches
-    assert fine.mode == "full"                     # b > 64: no eigen-split kernels in 3-D
+    assert fine.mode == "kron" and fine.tables.max_m == 588
+    b = random_rhs(op, 4)
+    x = np.random.default_rng(2).uniform(-1, 1, S.dim)
+    x[S.constrained_stage_dofs()] = 0.0
+    w = pat.pou_weights(op.dim)
+    assert rel(apply_vanka(fine, S, x, b, omega=0.4, weights="pou"),
+               oracle_apply_vanka(pat, op, x, b, 0.4, weights=w)) <= 1e-12
+
+
+@pytest.mark.parametrize("mode", ["kron", "full"])
+@pytest.mark.parametrize("fam", [("radauiia", 2), ("gauss", 2), ("lobattoiiic", 2)])
+def test_matvec_and_sweep_3d(fam, mode):
+    disc, tab, dt, mg, S, lv = _case(*fam, mode=mode)
+    op, pat = lv[-1]["op"], lv[-1]["patches"]
+    fine = mg.levels[-1].patches
+    assert fine.mode == mode
     x = np.random.default_rng(1).uniform(-1, 1, S.dim)
     x[S.constrained_stage_dofs()] = 0.0
     assert rel(S.matvec(x), op.matvec(x)) <= 1e-13
@@ -68,19 +85,22 @@ def test_matvec_and_sweep_3d(fam):
                oracle_apply_vanka(pat, op, x, b, 0.4, weights=w)) <= 1e-12
 
 
-def test_large_patch_inverses_3d():
-    """K7 (global Gauss-Jordan, d up to 392) against np.linalg.inv."""
-    disc, tab, dt, mg, S, lv = _case()
+@pytest.mark.parametrize("mode", ["kron", "full"])
+def test_large_patch_inverses_3d(mode):
+    """K7 (global Gauss-Jordan, d up to 392 / eigen-blocks b up to 196)
+    against np.linalg.inv."""
+    disc, tab, dt, mg, S, lv = _case(mode=mode)
     fine = mg.levels[-1].patches
     for (idx_d, inv_d), (idx_o, inv_o) in zip(fine.groups, lv[-1]["patches"].groups):
         assert np.array_equal(np.asarray(idx_d), idx_o)
         assert rel(np.asarray(inv_d), inv_o) <= 1e-12
 
 
+@pytest.mark.parametrize("pmode", ["kron", "full"])
 @pytest.mark.parametrize("mode", ["cheb", "pou"])
-def test_vcycle_3d(mode):
+def test_vcycle_3d(mode, pmode):
     from paper_2202_07381_b200 import MGHierarchyOp, MGLevel, SmootherSpec
-    disc, tab, dt, mg, S, lv = _case()
+    disc, tab, dt, mg, S, lv = _case(mode=pmode)
     if mode == "pou":
         sm = SmootherSpec(pre=2, post=2, accel="richardson", omega=0.4, weighting="pou")
         mg = MGHierarchyOp([MGLevel(l.system, l.patches, sm, l.prolong) for l in mg.levels],
