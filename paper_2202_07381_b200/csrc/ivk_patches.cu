@@ -552,7 +552,7 @@ static KronParams make_kron(const ivk_kron_desc* k, int S) {
 }
 
 __host__ __device__ __forceinline__ int kron_ldr(int b) { return (b + 3) & ~3; }
-__host__ __device__ __forceinline__ int kron_ldc(int b) { return (b + 1) & ~1; }
+__host__ __device__ __forceinline__ int kron_ldc(int b) { return (b + 3) & ~3; }  // 64-byte columns
 // symmetric storage: the lower tile-triangle of 4x4 tiles (I >= J, nt =
 // ceil(b/4)), ordered by tile diagonal d = I - J and, inside a diagonal,
 // chunk-major: the q-th 32-byte chunk of tile (d + t, t) at
