@@ -140,8 +140,8 @@ typedef struct ivk_patch_desc {
  * One block is stored per real eigenvalue and one per complex-conjugate pair
  * (the conjugate block is its complex conjugate).  Per patch, block k is
  * G_k^T (b = m / s rows): real blocks b x ldr doubles (ldr = (b+3)&~3),
- * complex blocks b x 2*ldc doubles, (re, im) interleaved (ldc = (b+3)&~3: every
- * column starts on a 64-byte DRAM granule).
+ * complex blocks b x 2*ldc doubles, (re, im) interleaved (ldc = (b+1)&~1 for
+ * b <= 64, else (b+3)&~3 so every column starts on a 64-byte DRAM granule).
  * Back-transform: z_i = sum_k scale_k Re(V[i][k] z~_k), scale 1 (real) or 2
  * (pair).  Inverse bytes per patch drop from (s b)^2 to s b^2 doubles. */
 typedef struct ivk_kron_desc {

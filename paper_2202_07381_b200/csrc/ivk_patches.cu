@@ -552,7 +552,13 @@ static KronParams make_kron(const ivk_kron_desc* k, int S) {
 }
 
 __host__ __device__ __forceinline__ int kron_ldr(int b) { return (b + 3) & ~3; }
-__host__ __device__ __forceinline__ int kron_ldc(int b) { return (b + 3) & ~3; }  // 64-byte columns
+// Complex columns: even length up to b = 64 (the narrow K3e / K3d layout the
+// cfg2 kernels are tuned on), then padded to 64-byte DRAM granules (b > 64:
+// MHD b = 78 -> 80, 3-D b = 176) so no granule straddles two columns.
+__host__ __device__ __forceinline__ int kron_ldc_narrow(int b) { return (b + 1) & ~1; }
+__host__ __device__ __forceinline__ int kron_ldc(int b) {
+  return b <= 64 ? kron_ldc_narrow(b) : (b + 3) & ~3;
+}
 // symmetric storage: the lower tile-triangle of 4x4 tiles (I >= J, nt =
 // ceil(b/4)), ordered by tile diagonal d = I - J and, inside a diagonal,
 // chunk-major: the q-th 32-byte chunk of tile (d + t, t) at
@@ -1103,7 +1109,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_kernel(
     for (int k = 0; k < kp.nblk; ++k) {
       double* rt = rt_all[warp][k];
       const bool cplx = kp.is_complex[k] != 0;
-      const int ldd = cplx ? 2 * kron_ldc(b) : kron_ldr(b);  // doubles per column
+      const int ldd = cplx ? 2 * kron_ldc_narrow(b) : kron_ldr(b);  // doubles per column
       const int cpc = ldd >> 2;                               // 32-byte chunks per column
       const int groups = 32 / cpc;
       const int g = lane / cpc, c = lane - g * cpc;
@@ -1178,7 +1184,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_kron_kernel(
           rt[2 * a] = re;
           rt[2 * a + 1] = im;
         }
-        G += 2L * b * kron_ldc(b);
+        G += 2L * b * kron_ldc_narrow(b);
       } else {
         for (int a = lane; a < b; a += 32) {
           const int ch = a >> 2, q = a & 3;
@@ -1494,10 +1500,10 @@ __global__ void __launch_bounds__(kClassWarps * 32, kClassCtas) patch_apply_clas
                      4 * RQ * li + 4 * (lane % RQ), 4 * (lane / RQ));
         } else {
           const int kc = (it - NR * ri) / ci, li = it - NR * ri - kc * ci;
-          const int goff = NR * b * kron_ldr(b) + kc * 2 * b * kron_ldc(b);
+          const int goff = NR * b * kron_ldr(b) + kc * 2 * b * kron_ldc_narrow(b);
           const int roff = (NR + 2 * kc) * b * T;
           const int rg = li / (T / 16), pg = li - rg * (T / 16);
-          cgemm_item(Gs + goff, Rs + roff, Zs + roff, b, kron_ldc(b), 8 * rg + 2 * (lane & 3),
+          cgemm_item(Gs + goff, Rs + roff, Zs + roff, b, kron_ldc_narrow(b), 8 * rg + 2 * (lane & 3),
                      16 * pg + 2 * (lane >> 2));
         }
       }
@@ -1786,7 +1792,7 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       dd.cdst = pd->cdst;
       int g = 0;
       for (int q = 0; q < k->nblk; ++q)
-        g += k->is_complex[q] ? 2 * bmax * kron_ldc(bmax) : bmax * kron_ldr(bmax);
+        g += k->is_complex[q] ? 2 * bmax * kron_ldc_narrow(bmax) : bmax * kron_ldr(bmax);
       g = ((g + 3) & ~3) + 32;  // slack: edge micro-tiles read past the last column
       const size_t smem = (size_t)(g + 2 * pd->max_m * kClassTile) * sizeof(double);
       int nr = 0;

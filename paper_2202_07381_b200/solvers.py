@@ -146,7 +146,7 @@ class KronSplit:
         if self.symmetric:
             return sum(self._sym_block(c, b) for c in self.is_complex)
         ldr = (b + 3) & ~3
-        ldc = (b + 3) & ~3
+        ldc = (b + 1) & ~1 if b <= 64 else (b + 3) & ~3
         return sum(2 * b * ldc if c else b * ldr for c in self.is_complex)
 
     @staticmethod
@@ -181,7 +181,7 @@ class KronSplit:
                 G.append(T[:b, :b])
                 pos += size
             elif cplx:
-                ldc = (b + 3) & ~3
+                ldc = (b + 1) & ~1 if b <= 64 else (b + 3) & ~3
                 a = raw[pos:pos + 2 * b * ldc].reshape(b, ldc, 2)[:, :b]
                 G.append((a[..., 0] + 1j * a[..., 1]).T)
                 pos += 2 * b * ldc
