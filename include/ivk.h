@@ -130,7 +130,33 @@ typedef struct ivk_patch_desc {
   const int32_t* tile_off;      /* n_tiles + 1 */
   const int32_t* cidx;          /* total_m     */
   const int32_t* cdst;          /* total_m     */
+  /* Modal store (non-NULL, HOST pointer; kron must be NULL): see
+   * ivk_modal_desc.  Patch p holds k = node_off[p+1] - node_off[p] free
+   * nodes and its record at inv_off[p]. */
+  const struct ivk_modal_desc* modal;
 } ivk_patch_desc;
+
+/* Modal split of Taylor-Hood (Stokes) patches.  The velocity blocks are
+ * M_s (x) I_nc and K_s (x) I_nc on the patch's k free scalar nodes,
+ * M_s symmetric positive definite, K_s symmetric, so one generalised
+ * eigendecomposition K_s W = M_s W Theta, W^T M_s W = I, diagonalises every
+ * stage and eigen-block at once.  With W = W_s (x) I_nc, c the patch's
+ * pressure column (B[vel, v]) and c^ = W^T c, the stage-coupled patch system
+ *   sum_b [delta_ab M + dt A_ab K] u_b + dt A_ab c p_b = r_a,
+ *   sum_b dt A_ab c^T u_b = q_a
+ * becomes, per mode (i, d) with E_i = (I_s + dt theta_i A)^-1 (s x s):
+ *   t = W^T r,  w_id = E_i t_id,  g = sum_id c^_id w_id,
+ *   p = H^-1 (dt A g - q),  H = dt^2 A (sum_id c^_id^2 E_i) A,
+ *   v_id = w_id - dt c^_id E_i A p,  u = W v.
+ * Exactly the inverse of R_i A R_i^T (solvers.py:186-212; any tableau).
+ * Record of a patch (doubles, padded to a multiple of 4):
+ *   W_s[alpha][i] row-major (k x k) | theta (k) | c^[i][d] (k x nc) | H^-1 (s x s). */
+typedef struct ivk_modal_desc {
+  int32_t stages;
+  int32_t ncomp;
+  double dt;
+  double butcher_a[IVK_MAX_STAGES * IVK_MAX_STAGES];
+} ivk_modal_desc;
 
 /* Kronecker eigen-split of the patch matrices.  With all stages sharing one
  * convection Jacobian the stage-coupled patch matrix is
@@ -250,6 +276,13 @@ int ivk_index_copy(int64_t n, const int32_t* src_idx, const double* src, const i
                    double* dst, double beta, void* stream);
 int ivk_index_update(int64_t n, const int32_t* idx, double alpha, const double* x, double beta,
                      const double* w, const double* z, double* out, void* stream);
+
+/* Modal-split setup input: for every patch p the k x k scalar blocks
+ * Ms[p][alpha][beta] = M_s, Ks[p][alpha][beta] = K_s (zero padded to kmax x
+ * kmax) and C[p][alpha][d] = B[nc alpha + d, vertex] (kmax x nc), gathered
+ * from the eliminated operator (solvers.py:190-194).  Stokes only (n_conv = 0). */
+int ivk_patch_gather_blocks(const ivk_operator_desc* op, const ivk_patch_desc* pd, int32_t kmax,
+                            double* Ms, double* Ks, double* C, void* stream);
 
 /* Assemble every patch matrix from the operator (solvers.py:186-212) and
  * invert it in place into pd->inv (np.linalg.inv, solvers.py:177) by

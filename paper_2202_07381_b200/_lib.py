@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 __all__ = ["lib", "check", "OperatorDesc", "PatchDesc", "KronDesc", "TransferDesc", "CoarseDesc",
-           "GeneralDesc", "GeneralTransferDesc",
+           "GeneralDesc", "GeneralTransferDesc", "ModalDesc",
            "IVK_MAX_STAGES", "IvkError", "SingularPatch"]
 
 IVK_MAX_STAGES = 3
@@ -64,6 +64,13 @@ class KronDesc(C.Structure):
     ]
 
 
+class ModalDesc(C.Structure):
+    _fields_ = [
+        ("stages", C.c_int32), ("ncomp", C.c_int32), ("dt", C.c_double),
+        ("butcher_a", C.c_double * (IVK_MAX_STAGES * IVK_MAX_STAGES)),
+    ]
+
+
 class PatchDesc(C.Structure):
     _fields_ = [
         ("num_patches", C.c_int32), ("dim", C.c_int32), ("max_m", C.c_int32),
@@ -77,6 +84,7 @@ class PatchDesc(C.Structure):
         ("class_inv_off", C.c_void_p), ("class_inv", C.c_void_p),
         ("n_tiles", C.c_int32), ("tile_start", C.c_void_p), ("tile_class", C.c_void_p),
         ("tile_off", C.c_void_p), ("cidx", C.c_void_p), ("cdst", C.c_void_p),
+        ("modal", C.POINTER(ModalDesc)),
     ]
 
 
@@ -176,6 +184,8 @@ _SIGS = {
     "ivk_mgs": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P, _P], C.c_int),
     "ivk_scale": ([C.c_int64, _P, _P, C.c_int32, _P, _P], C.c_int),
     "ivk_lincomb": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P], C.c_int),
+    "ivk_patch_gather_blocks": ([C.POINTER(OperatorDesc), C.POINTER(PatchDesc), C.c_int32, _P,
+                                 _P, _P, _P], C.c_int),
     "ivk_general_apply": ([C.POINTER(GeneralDesc), _P, _P, _P, _P], C.c_int),
     "ivk_general_patch_factor": ([C.POINTER(GeneralDesc), C.POINTER(PatchDesc), _P, _P], C.c_int),
     "ivk_general_vanka_sweep": ([C.POINTER(GeneralDesc), C.POINTER(PatchDesc), _P, _P, C.c_double,

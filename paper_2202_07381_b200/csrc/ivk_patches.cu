@@ -949,6 +949,356 @@ __global__ void __launch_bounds__(kFactorGlobalThreads) patch_factor_kron_global
   }
 }
 
+// ------------------------------------------------------------ modal split
+//
+// K7m input (ivk_patch_gather_blocks): the scalar M_s, K_s blocks and the
+// pressure column of every patch, gathered from the eliminated operator on
+// the patch's free nodes (the same lookups as K7); the generalised
+// eigendecomposition itself runs at setup on the device (solvers.py
+// ModalSplit).  K3m (patch_apply_modal_kernel): warp per patch, the record
+// W_s | theta | c^ | H^-1 staged in shared memory (W_s with an odd leading
+// dimension, so both W^T r and W v read it conflict-free), r_p gathered once;
+// t = W^T r, per-mode s x s solves, one warp reduction for the pressure
+// Schur complement, u = W v.  Bytes per patch: (k^2 + (1 + nc) k + s^2)
+// doubles instead of s b^2 (kron) or (s b)^2 (full).
+
+struct ModalParams {
+  int S, NC;
+  double dt;
+  double a[IVK_MAX_STAGES * IVK_MAX_STAGES];
+};
+
+// record: W_s rows with odd leading dimension k|1 (the shared-memory layout,
+// so one TMA bulk copy lands it ready to use), theta, c^, H^-1; 32-byte padded
+__host__ __device__ __forceinline__ int modal_rec(int S, int NC, int k) {
+  return (k * (k | 1) + k + NC * k + S * S + 3) & ~3;
+}
+// per warp: two record buffers (double-buffered bulk copies), two r_p buffers
+// (the next patch's gather is prefetched), t, E
+__host__ __device__ __forceinline__ int modal_seg(int S, int NC, int kmax) {
+  const int NA = NC * S;
+  return (2 * modal_rec(S, NC, kmax) + 2 * ((kmax * NA + S + 1) & ~1) + kmax * NA +
+          kmax * S * S + 3) & ~3;  // 32-byte aligned (TMA destinations, 16-byte smem vector loads)
+}
+
+template <int NC>
+__global__ void __launch_bounds__(128) patch_gather_blocks_kernel(FactorParams op, PatchParams pd,
+                                                                  int kmax, double* __restrict__ Ms,
+                                                                  double* __restrict__ Ks,
+                                                                  double* __restrict__ Cb) {
+  const int p = blockIdx.x;
+  const int n0 = pd.node_off[p], nk = pd.node_off[p + 1] - n0;
+  const int* nodes = pd.node + n0;
+  const int v = pd.vertex[p];
+  double* ms = Ms + (long)p * kmax * kmax;
+  double* ks = Ks + (long)p * kmax * kmax;
+  double* cb = Cb + (long)p * kmax * NC;
+  for (int e = threadIdx.x; e < kmax * kmax; e += blockDim.x) {
+    const int al = e / kmax, be = e - al * kmax;
+    double m = 0.0, k = 0.0;
+    if (al < nk && be < nk) {
+      const int row = nodes[al];
+      const int pos = find_col(op.p2_col, op.p2_rowptr[row], op.p2_rowptr[row + 1], nodes[be]);
+      if (pos >= 0) {
+        const double2 mk = op.p2_mk[pos];
+        m = mk.x;
+        k = mk.y;
+      }
+    }
+    ms[e] = m;
+    ks[e] = k;
+  }
+  for (int al = threadIdx.x; al < kmax; al += blockDim.x) {
+    int pos = -1;
+    if (al < nk) {
+      const int row = nodes[al];
+      pos = find_col(op.b_col, op.b_rowptr[row], op.b_rowptr[row + 1], v);
+    }
+    for (int d = 0; d < NC; ++d) cb[al * NC + d] = pos >= 0 ? op.b_raw[(long)pos * NC + d] : 0.0;
+  }
+}
+
+// E = (I + f A)^-1 for s <= 3 (explicit adjugate: I + f A is well
+// conditioned for f = dt theta >= 0 and A with eigenvalues in the right
+// half plane -- every tableau the library builds).
+template <int S>
+__device__ __forceinline__ void modal_small_inv(const double* A, double f, double* E) {
+  double m[S * S];
+#pragma unroll
+  for (int i = 0; i < S; ++i)
+#pragma unroll
+    for (int j = 0; j < S; ++j) m[i * S + j] = (i == j ? 1.0 : 0.0) + f * A[i * S + j];
+  if constexpr (S == 1) {
+    E[0] = 1.0 / m[0];
+  } else if constexpr (S == 2) {
+    const double id = 1.0 / (m[0] * m[3] - m[1] * m[2]);
+    E[0] = m[3] * id;
+    E[1] = -m[1] * id;
+    E[2] = -m[2] * id;
+    E[3] = m[0] * id;
+  } else {
+    const double c00 = m[4] * m[8] - m[5] * m[7];
+    const double c01 = m[5] * m[6] - m[3] * m[8];
+    const double c02 = m[3] * m[7] - m[4] * m[6];
+    const double id = 1.0 / (m[0] * c00 + m[1] * c01 + m[2] * c02);
+    E[0] = c00 * id;
+    E[1] = (m[2] * m[7] - m[1] * m[8]) * id;
+    E[2] = (m[1] * m[5] - m[2] * m[4]) * id;
+    E[3] = c01 * id;
+    E[4] = (m[0] * m[8] - m[2] * m[6]) * id;
+    E[5] = (m[2] * m[3] - m[0] * m[5]) * id;
+    E[6] = c02 * id;
+    E[7] = (m[1] * m[6] - m[0] * m[7]) * id;
+    E[8] = (m[0] * m[4] - m[1] * m[3]) * id;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void lds_vec(const double* p, double (&v)[N]) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int q = 0; q < N; q += 2) {
+      const double2 x = *reinterpret_cast<const double2*>(p + q);
+      v[q] = x.x;
+      v[q + 1] = x.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < N; ++q) v[q] = p[q];
+  }
+}
+
+template <int S, int NC>
+__global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_kernel(
+    PatchParams pd, ModalParams mp, const double* __restrict__ r, double* __restrict__ local,
+    int kmax) {
+  extern __shared__ __align__(16) double modal_sm[];
+  __shared__ __align__(8) uint64_t bars[kApplyWarps][2];
+  constexpr int NA = NC * S;  // (component, stage) pairs per mode / node
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int recmax = modal_rec(S, NC, kmax);
+  double* buf0 = modal_sm + (long)warp * modal_seg(S, NC, kmax);
+  double* buf1 = buf0 + recmax;
+  const int rsn = (kmax * NA + S + 1) & ~1;
+  double* rsT0 = buf1 + recmax;                // r_p: [alpha][d][a], then the s pressures
+  double* rsT1 = rsT0 + rsn;                   // (double-buffered: next patch prefetched)
+  double* t = rsT1 + rsn;                      // W^T r, then w, then v: [i][d][a]
+  double* Es = t + kmax * NA;                  // E_i = (I + dt theta_i A)^-1
+  if (lane == 0) {
+    mbar_init(&bars[warp][0], 1);
+    mbar_init(&bars[warp][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  double A[S * S];
+#pragma unroll
+  for (int e = 0; e < S * S; ++e) A[e] = mp.a[e];
+  const double dt = mp.dt;
+  const int stride = gridDim.x * nw;
+  int p = blockIdx.x * nw + warp;
+  // one TMA bulk copy per patch record, one record ahead of the compute
+  if (lane == 0 && p < pd.num_patches) {
+    const int k0 = pd.node_off[p + 1] - pd.node_off[p];
+    bulk_load(buf0, pd.inv + pd.inv_off[p], modal_rec(S, NC, k0) * 8, &bars[warp][0]);
+  }
+  if (p < pd.num_patches) {
+    const int off0 = pd.idx_off[p];
+    const int k0 = pd.node_off[p + 1] - pd.node_off[p];
+    const int blk0 = NC * k0 + 1;
+    for (int j = lane; j < S * blk0 && j < 128; j += 32) {
+      const int a = (j >= blk0) + (S > 2 && j >= 2 * blk0);
+      const int e = j - a * blk0;
+      const double v = __ldg(r + pd.idx[off0 + j]);
+      if (e < NC * k0) {
+        const int al = e / NC, d = e - al * NC;
+        rsT0[al * NA + d * S + a] = v;
+      } else {
+        rsT0[k0 * NA + a] = v;
+      }
+    }
+  }
+  uint32_t phase = 0;
+  for (int it = 0; p < pd.num_patches; ++it, p += stride) {
+    const int slot = it & 1;
+    const int pn = p + stride;
+    if (lane == 0 && pn < pd.num_patches) {
+      const int kn = pd.node_off[pn + 1] - pd.node_off[pn];
+      bulk_load(slot ? buf0 : buf1, pd.inv + pd.inv_off[pn], modal_rec(S, NC, kn) * 8,
+                &bars[warp][slot ^ 1]);
+    }
+    const int off = pd.idx_off[p];
+    const int k = pd.node_off[p + 1] - pd.node_off[p];
+    const int blk = NC * k + 1;
+    const int ld = k | 1;
+    // r_p: the first 128 entries were prefetched into registers during the
+    // previous patch (pf); the rest (3-D patches) are gathered here
+    double* rsT = slot ? rsT1 : rsT0;
+    for (int j = 128 + lane; j < S * blk; j += 32) {
+      const int a = (j >= blk) + (S > 2 && j >= 2 * blk);
+      const int e = j - a * blk;
+      const double v = __ldg(r + pd.idx[off + j]);
+      if (e < NC * k) {
+        const int al = e / NC, d = e - al * NC;
+        rsT[al * NA + d * S + a] = v;
+      } else {
+        rsT[k * NA + a] = v;
+      }
+    }
+    // next patch: its gather indices now, its r values after step 1
+    int pf_idx[4];
+    int pn_off = 0, pn_k = 0, pn_blk = 0;
+    if (pn < pd.num_patches) {
+      pn_off = pd.idx_off[pn];
+      pn_k = pd.node_off[pn + 1] - pd.node_off[pn];
+      pn_blk = NC * pn_k + 1;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = lane + 32 * u;
+      pf_idx[u] = (pn < pd.num_patches && j < S * pn_blk) ? __ldg(pd.idx + pn_off + j) : -1;
+    }
+    mbar_wait(&bars[warp][slot], (phase >> slot) & 1u);
+    phase ^= 1u << slot;
+    __syncwarp();
+    const double* W = slot ? buf1 : buf0;
+    const double* th = W + k * ld;
+    const double* ch = th + k;
+    const double* hi = ch + NC * k;
+    // lane per mode i: t_i = W^T r for every (d, a) at once, w_i = E_i t_i,
+    // g += c^ w
+    double g[S];
+#pragma unroll
+    for (int a = 0; a < S; ++a) g[a] = 0.0;
+    for (int i = lane; i < k; i += 32) {
+      double acc[NA];
+#pragma unroll
+      for (int q = 0; q < NA; ++q) acc[q] = 0.0;
+      for (int al = 0; al < k; ++al) {
+        const double w = W[al * ld + i];
+        double rr[NA];
+        lds_vec<NA>(rsT + al * NA, rr);
+#pragma unroll
+        for (int q = 0; q < NA; ++q) acc[q] = fma(w, rr[q], acc[q]);
+      }
+      double E[S * S];
+      modal_small_inv<S>(A, dt * th[i], E);
+#pragma unroll
+      for (int e = 0; e < S * S; ++e) Es[i * S * S + e] = E[e];
+#pragma unroll
+      for (int d = 0; d < NC; ++d) {
+        const double c = ch[i * NC + d];
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+          double w = 0.0;
+#pragma unroll
+          for (int b = 0; b < S; ++b) w = fma(E[a * S + b], acc[d * S + b], w);
+          t[i * NA + d * S + a] = w;
+          g[a] = fma(c, w, g[a]);
+        }
+      }
+    }
+    double pf_val[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) pf_val[u] = pf_idx[u] >= 0 ? __ldg(r + pf_idx[u]) : 0.0;
+    // fixed-order tree to lane 0, then broadcast (every lane the same bits)
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) g[a] += __shfl_down_sync(0xffffffffu, g[a], o);
+      g[a] = __shfl_sync(0xffffffffu, g[a], 0);
+    }
+    // p = H^-1 (dt A g - q),  Ap = A p
+    double rhs[S], pv[S], Ap[S];
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+      double s_ = 0.0;
+#pragma unroll
+      for (int b = 0; b < S; ++b) s_ = fma(A[a * S + b], g[b], s_);
+      rhs[a] = dt * s_ - rsT[k * NA + a];
+    }
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+      double s_ = 0.0;
+#pragma unroll
+      for (int b = 0; b < S; ++b) s_ = fma(hi[a * S + b], rhs[b], s_);
+      pv[a] = s_;
+    }
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+      double s_ = 0.0;
+#pragma unroll
+      for (int b = 0; b < S; ++b) s_ = fma(A[a * S + b], pv[b], s_);
+      Ap[a] = s_;
+    }
+    // v_i = w_i - dt c^ E_i A p  (each lane rewrites its own modes)
+    for (int i = lane; i < k; i += 32) {
+      double e[S];
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        double s_ = 0.0;
+#pragma unroll
+        for (int b = 0; b < S; ++b) s_ = fma(Es[i * S * S + a * S + b], Ap[b], s_);
+        e[a] = s_;
+      }
+#pragma unroll
+      for (int d = 0; d < NC; ++d) {
+        const double c = dt * ch[i * NC + d];
+#pragma unroll
+        for (int a = 0; a < S; ++a) t[i * NA + d * S + a] = fma(-c, e[a], t[i * NA + d * S + a]);
+      }
+    }
+    __syncwarp();
+    // lane per node alpha: u[a][NC alpha + d] = sum_i W[alpha][i] v[i][d][a]
+    for (int al = lane; al < k; al += 32) {
+      double acc[NA];
+#pragma unroll
+      for (int q = 0; q < NA; ++q) acc[q] = 0.0;
+      const double* wr = W + al * ld;
+      for (int i = 0; i < k; ++i) {
+        const double w = wr[i];
+        double vv[NA];
+        lds_vec<NA>(t + i * NA, vv);
+#pragma unroll
+        for (int q = 0; q < NA; ++q) acc[q] = fma(w, vv[q], acc[q]);
+      }
+#pragma unroll
+      for (int d = 0; d < NC; ++d)
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+          const int pos = off + a * blk + NC * al + d;
+          st_keep(local + (pd.slot_pos ? pd.slot_pos[pos] : pos), acc[d * S + a]);
+        }
+    }
+    if (lane < S) {
+      const int pos = off + lane * blk + NC * k;
+      double pl = pv[0];
+#pragma unroll
+      for (int a = 1; a < S; ++a)
+        if (lane == a) pl = pv[a];
+      st_keep(local + (pd.slot_pos ? pd.slot_pos[pos] : pos), pl);
+    }
+    // land the next patch's prefetched r values
+    {
+      double* rsN = slot ? rsT0 : rsT1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = lane + 32 * u;
+        if (pf_idx[u] >= 0) {
+          const int a = (j >= pn_blk) + (S > 2 && j >= 2 * pn_blk);
+          const int e = j - a * pn_blk;
+          if (e < NC * pn_k) {
+            const int al = e / NC, d = e - al * NC;
+            rsN[al * NA + d * S + a] = pf_val[u];
+          } else {
+            rsN[pn_k * NA + a] = pf_val[u];
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------------- K7g (general path)
 //
 // One CTA per patch of a general stage operator I_s (x) M + dt A (x) L
@@ -1739,6 +2089,47 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
   const int cap = kSMs * 8;  // persistent-ish: 8 CTAs (64 warps) per SM
   if (grid > cap) grid = cap;
   cudaStream_t st = as_stream(stream);
+  if (pd->modal) {
+    const ivk_modal_desc* md = pd->modal;
+    IVK_REQUIRE(pd->node_off != nullptr, "modal store needs the per-patch node counts");
+    IVK_REQUIRE(md->stages >= 1 && md->stages <= IVK_MAX_STAGES && (md->ncomp == 2 || md->ncomp == 3),
+                "bad modal descriptor");
+    ModalParams mp;
+    mp.S = md->stages;
+    mp.NC = md->ncomp;
+    mp.dt = md->dt;
+    for (int i = 0; i < IVK_MAX_STAGES * IVK_MAX_STAGES; ++i) mp.a[i] = md->butcher_a[i];
+    const int kmax = (pd->max_m / md->stages - 1) / md->ncomp;
+    const size_t seg = (size_t)modal_seg(mp.S, mp.NC, kmax) * sizeof(double);
+    // warps per CTA: three CTAs per SM when the per-warp buffers allow it
+    int nw = (int)((72 * 1024) / seg);
+    if (nw > kApplyWarps) nw = kApplyWarps;
+    if (nw < 1) nw = 1;
+    IVK_REQUIRE(seg <= 200 * 1024, "modal patch (k = %d) exceeds shared memory", kmax);
+    const size_t smem = seg * nw;
+    void (*fn)(PatchParams, ModalParams, const double*, double*, int) = nullptr;
+    if (mp.NC == 2) {
+      if (mp.S == 1) fn = patch_apply_modal_kernel<1, 2>;
+      else if (mp.S == 2) fn = patch_apply_modal_kernel<2, 2>;
+      else fn = patch_apply_modal_kernel<3, 2>;
+    } else {
+      if (mp.S == 1) fn = patch_apply_modal_kernel<1, 3>;
+      else if (mp.S == 2) fn = patch_apply_modal_kernel<2, 3>;
+      else fn = patch_apply_modal_kernel<3, 3>;
+    }
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) {
+        set_error("ivk_patch_apply: %s", cudaGetErrorString(e));
+        return IVK_ECUDA;
+      }
+    }
+    int mgrid = (pd->num_patches + nw - 1) / nw;
+    const int cap = kSMs * 3;
+    if (mgrid > cap) mgrid = cap;
+    fn<<<mgrid, nw * 32, smem, st>>>(p, mp, r, local, kmax);
+    return check_launch("ivk_patch_apply(modal)");
+  }
   if (pd->kron) {
     const ivk_kron_desc* k = pd->kron;
     IVK_REQUIRE(k->nblk >= 1 && k->nblk <= IVK_MAX_STAGES, "bad kron block count");
@@ -1954,6 +2345,24 @@ int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int3
   patch_factor_kernel<<<pd->num_patches, kFactorThreads, smem, as_stream(stream)>>>(f, p,
                                                                                     singular_dev);
   return check_launch("ivk_patch_factor");
+}
+
+int ivk_patch_gather_blocks(const ivk_operator_desc* op, const ivk_patch_desc* pd, int32_t kmax,
+                            double* Ms, double* Ks, double* C, void* stream) {
+  int rc = validate_op(op);
+  if (rc) return rc;
+  rc = validate_patches(pd);
+  if (rc) return rc;
+  IVK_REQUIRE(pd->vertex && pd->node_off && pd->node && Ms && Ks && C && kmax >= 1,
+              "gather needs vertex/node tables and output buffers");
+  IVK_REQUIRE(op->n_conv == 0, "the modal split needs a convection-free (symmetric) operator");
+  FactorParams f = make_factor_params(op);
+  PatchParams p = make_patch_params(pd);
+  if (f.ncomp == 3)
+    patch_gather_blocks_kernel<3><<<pd->num_patches, 128, 0, as_stream(stream)>>>(f, p, kmax, Ms, Ks, C);
+  else
+    patch_gather_blocks_kernel<2><<<pd->num_patches, 128, 0, as_stream(stream)>>>(f, p, kmax, Ms, Ks, C);
+  return check_launch("ivk_patch_gather_blocks");
 }
 
 int ivk_general_patch_factor(const ivk_general_desc* op, const ivk_patch_desc* pd,

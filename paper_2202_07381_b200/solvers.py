@@ -240,8 +240,15 @@ class VankaPatchSet:
                                              system.node_constrained, vertices=vertices,
                                              ncomp=system.nc)
         self.num_patches = self.tables.num_patches
-        if mode not in ("auto", "full", "kron", "kron-sym", "dedup"):
+        if mode not in ("auto", "full", "kron", "kron-sym", "dedup", "modal"):
             raise ValueError(f"unknown patch mode {mode!r}")
+        self.modal = None
+        if mode == "modal":
+            # Stokes only: velocity blocks M_s (x) I and K_s (x) I, K_s symmetric
+            if self.general or system.convection is not None:
+                raise ValueError("modal split needs a convection-free Taylor-Hood operator")
+            from .modal import ModalSplit
+            self.modal = ModalSplit(system.tableau, system.dt, system.nc)
         # kron-sym halves the inverse bytes but measures no faster than kron on
         # B200 (latency-bound, profiles/r01): "auto" keeps the plain kron layout.
         symmetric = mode == "kron-sym"
@@ -283,7 +290,7 @@ class VankaPatchSet:
             dd = build_dedup_tables(mesh, system, self.tables)
             if mode == "dedup" or dd.n_classes * 8 <= self.tables.num_patches:
                 self.dedup = dd
-        self.mode = "full" if self.kron is None else \
+        self.mode = "modal" if self.modal is not None else "full" if self.kron is None else \
             ("dedup" if self.dedup is not None else
              ("kron-sym" if self.kron.symmetric else "kron"))
         self._layout()
@@ -294,6 +301,12 @@ class VankaPatchSet:
 
     def _layout(self):
         t = self.tables
+        if self.modal is not None:
+            ks = np.diff(t.node_off).astype(np.int64)
+            sizes = np.array([self.modal.record_doubles(int(k)) for k in ks], dtype=np.int64)
+            off = np.concatenate([[0], np.cumsum(sizes)])
+            self.inv_off, self.inv_size = off[:-1], int(off[-1])
+            return
         if self.dedup is not None:
             # per-class (representative) inverse blocks only
             sizes = np.array([self.kron.block_doubles(int(t.sizes[q]) // t.stages)
@@ -340,6 +353,19 @@ class VankaPatchSet:
         dev = self.device_data()
         inv_all = dev["inv"]
         out = []
+        if self.modal is not None:
+            raw = inv_all.cpu().numpy()
+            ks = np.diff(t.node_off)
+            for m, first, count in t.groups():
+                idx = t.idx[t.idx_off[first]:t.idx_off[first + count]].reshape(count, m)
+                inv = np.empty((count, m, m))
+                for qq in range(count):
+                    q = first + qq
+                    o = int(self.inv_off[q])
+                    inv[qq] = self.modal.full_inverse(raw[o:o + self.modal.record_doubles(int(ks[q]))],
+                                                      int(ks[q]))
+                out.append((idx.copy(), inv))
+            return out
         if self.dedup is not None:
             dd = self.dedup
             raw = inv_all.cpu().numpy()
@@ -425,6 +451,9 @@ class VankaPatchSet:
         if self.kron is not None:
             d["kron"] = self.kron.desc()          # keep the host struct alive
             desc.kron = C.pointer(d["kron"])
+        if self.modal is not None:
+            d["modal"] = self.modal.desc()
+            desc.modal = C.pointer(d["modal"])
         if self.dedup is not None:
             dd = self.dedup
             # canonical gather list and write positions, in tile (class) order
@@ -484,6 +513,12 @@ class VankaPatchSet:
         dev = self.device_data()
         flag = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev["idx"].device)
         target = dev["rep_desc"] if self.dedup is not None else dev["desc"]
+        if self.modal is not None:
+            bad = self.modal.factor(self)
+            if bad:
+                raise PatchSingularError(int(min(self.tables.order[b] for b in bad)))
+            self._factored = True
+            return
         if self.general:
             self.system.factor_patches(target, flag)
         else:
@@ -499,8 +534,9 @@ class VankaPatchSet:
         format [(idx (P,m), inv (P,m,m))] instead of factorising on the GPU."""
         import torch
         t = self.tables
-        if self.kron is not None:       # reference inverses are full (s b)^2 blocks
+        if self.kron is not None or self.modal is not None:   # reference inverses are full
             self.kron = None
+            self.modal = None
             self.dedup = None
             self.mode = "full"
             self._layout()

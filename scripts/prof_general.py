@@ -2,7 +2,7 @@
 hierarchy exactly as bench.py does (patch_mode="kron"), then run N sweeps
 K1 (K1g for MHD) -> K3e (wide) -> K4 with CUDA-event timings printed.
 
-    python scripts/prof_general.py cfg5 [sweeps]
+    python scripts/prof_general.py cfg5 [sweeps] [patch_mode]
 """
 import os
 import sys
@@ -17,10 +17,10 @@ from paper_2202_07381_b200 import SmootherSpec, _lib  # noqa: E402
 from paper_2202_07381_b200._device import ptr, stream  # noqa: E402
 
 
-def main(name, n):
+def main(name, n, mode="kron"):
     cfg = bench.CONFIGS[name]
     disc, tab, conv = bench.make_disc(cfg)
-    mg, S = disc.build_mg(tab, cfg["dt"], SmootherSpec(), convection=conv, patch_mode="kron")
+    mg, S = disc.build_mg(tab, cfg["dt"], SmootherSpec(), convection=conv, patch_mode=mode)
     pat = mg.levels[-1].patches
     dev = pat.device_data()
     b_h = np.random.default_rng(cfg["seed"]).uniform(-1, 1, S.dim)
@@ -53,4 +53,5 @@ def main(name, n):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 6)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 6,
+         sys.argv[3] if len(sys.argv) > 3 else "kron")

@@ -47,6 +47,7 @@ STRUCTS = {
     "ivk_convection_desc": _lib.ConvectionDesc,
     "ivk_general_desc": _lib.GeneralDesc,
     "ivk_general_transfer_desc": _lib.GeneralTransferDesc,
+    "ivk_modal_desc": _lib.ModalDesc,
 }
 
 

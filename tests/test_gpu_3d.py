@@ -66,7 +66,7 @@ def test_three_stage_3d_kron():
                oracle_apply_vanka(pat, op, x, b, 0.4, weights=w)) <= 1e-12
 
 
-@pytest.mark.parametrize("mode", ["kron", "full"])
+@pytest.mark.parametrize("mode", ["kron", "full", "modal"])
 @pytest.mark.parametrize("fam", [("radauiia", 2), ("gauss", 2), ("lobattoiiic", 2)])
 def test_matvec_and_sweep_3d(fam, mode):
     disc, tab, dt, mg, S, lv = _case(*fam, mode=mode)
@@ -85,7 +85,7 @@ def test_matvec_and_sweep_3d(fam, mode):
                oracle_apply_vanka(pat, op, x, b, 0.4, weights=w)) <= 1e-12
 
 
-@pytest.mark.parametrize("mode", ["kron", "full"])
+@pytest.mark.parametrize("mode", ["kron", "full", "modal"])
 def test_large_patch_inverses_3d(mode):
     """K7 (global Gauss-Jordan, d up to 392 / eigen-blocks b up to 196)
     against np.linalg.inv."""
@@ -96,7 +96,7 @@ def test_large_patch_inverses_3d(mode):
         assert rel(np.asarray(inv_d), inv_o) <= 1e-12
 
 
-@pytest.mark.parametrize("pmode", ["kron", "full"])
+@pytest.mark.parametrize("pmode", ["kron", "full", "modal"])
 @pytest.mark.parametrize("mode", ["cheb", "pou"])
 def test_vcycle_3d(mode, pmode):
     from paper_2202_07381_b200 import MGHierarchyOp, MGLevel, SmootherSpec

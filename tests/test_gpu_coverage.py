@@ -155,3 +155,23 @@ def test_residual_in_place_matches(name):
     _lib.check(L.ivk_stage_apply(S.desc, ptr(x), ptr(bb), ptr(bb), stream()), "K1")
     assert torch.equal(r, bb)
     assert rel(r.cpu().numpy(), b.cpu().numpy() - S.matvec(x.cpu().numpy())) <= 1e-13
+
+
+@pytest.mark.parametrize("family,stages", [("dirk-pareschirusso", 2), ("lobattoiiic", 3),
+                                           ("backwardeuler", 1), ("gauss", 3)])
+def test_modal_any_tableau(family, stages):
+    """The modal split needs no eigen-split of A: non-diagonalisable DIRK
+    tableaux run through it too (sweep parity against the full inverses)."""
+    import torch
+    from paper_2202_07381_b200 import SmootherSpec, VankaPatchSet, apply_vanka, tableau_lookup
+    disc = _disc()
+    tab = tableau_lookup(family, stages)
+    mg, S = disc.build_mg(tab, 1.0 / 16, SmootherSpec(), patch_mode="modal")
+    fine = mg.levels[-1].patches
+    assert fine.mode == "modal"
+    full = VankaPatchSet(S, disc.fine_mesh, mode="full")
+    b = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, S.dim)).cuda()
+    x0 = torch.zeros_like(b)
+    ym = apply_vanka(fine, S, x0, b, omega=0.5, weights="pou")
+    yf = apply_vanka(full, S, x0, b, omega=0.5, weights="pou")
+    assert float(torch.linalg.vector_norm(ym - yf)) <= 1e-12 * float(torch.linalg.vector_norm(yf))

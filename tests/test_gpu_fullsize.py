@@ -147,7 +147,7 @@ def test_patch_formulations_agree(full):
     assert kron.mode == ("kron" if conv is not None else "dedup")
     x0 = torch.zeros_like(b)
     yk = apply_vanka(kron, S, x0, b, omega=0.5, weights="pou")
-    for mode in (["full"] if conv is not None else ["full", "kron", "kron-sym"]):
+    for mode in (["full"] if conv is not None else ["full", "kron", "kron-sym", "modal"]):
         other = VankaPatchSet(S, disc.fine_mesh, mode=mode)
         yo = apply_vanka(other, S, x0, b, omega=0.5, weights="pou")
         del other

@@ -49,11 +49,12 @@ class Case:
 _cache = {}
 
 
-@pytest.fixture(params=[(n, m) for n in CASES for m in ("auto", "kron-sym", "dedup", "full")],
+@pytest.fixture(params=[(n, m) for n in CASES
+                        for m in ("auto", "kron-sym", "dedup", "full", "modal")],
                 ids=lambda p: f"{p[0]}-{p[1]}")
 def case(request):
-    if request.param in (("ns", "kron-sym"), ("ns", "dedup")):
-        pytest.skip("kron-sym / dedup need a convection-free operator")
+    if request.param in (("ns", "kron-sym"), ("ns", "dedup"), ("ns", "modal")):
+        pytest.skip("kron-sym / dedup / modal need a convection-free operator")
     if request.param not in _cache:
         _cache.clear()   # one case resident at a time
         _cache[request.param] = Case(*request.param)
