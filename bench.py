@@ -6,7 +6,10 @@ Workload (BASELINE config 2, the headline): 256x256 right-triangle grid
 nu=1; RHS uniform[-1,1] seed 1 (constrained rows zeroed, pressure means
 removed).  One STEP = one fine-level additive Vanka sweep
 x <- x + 0.5 W sum_i R_i^T A_i^-1 R_i (b - A x) (PoU weights W: the
-BASELINE "damping 0.5" smoother), i.e. kernels K1 -> K3 -> K4.
+BASELINE "damping 0.5" smoother), i.e. kernels K1 -> K3 -> K4,
+with the patch inverses in the modal split (modal.py) on Stokes configs and
+the Butcher eigen-split (kron) elsewhere; the other formulations are timed
+beside it (``formulations``).
 
 value = sweeps/s over all ranks (weak scaling: every rank runs a replica);
 also reported: stage-DOF updates/s, the V-cycle time (both smoothers), the
@@ -359,9 +362,13 @@ def run_ours(args, rank, world, local):
     is_mhd = cfg["grid"] == "mhd"
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    # the headline sweep runs the general per-patch formulation (kron: every
-    # patch streams its own eigen-split inverse blocks from HBM)
-    mg, S = disc.build_mg(tab, cfg["dt"], cheb, convection=conv, patch_mode="kron")
+    # the headline sweep runs a per-patch formulation valid on any mesh:
+    # "modal" (Stokes: per-patch generalised eigenbasis, modal.py) on the 2-D
+    # Stokes configs, "kron" (Butcher eigen-split blocks) where a convection or
+    # a general multi-field operator breaks the M_s (x) I / K_s (x) I structure
+    # and for 3-D (its modal kernel is not tuned yet)
+    head = "modal" if (conv is None and not is3d and not is_mhd) else "kron"
+    mg, S = disc.build_mg(tab, cfg["dt"], cheb, convection=conv, patch_mode=head)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     pou = SmootherSpec(pre=2, post=2, accel="richardson", omega=om, weighting="pou")
@@ -498,7 +505,7 @@ def run_ours(args, rank, world, local):
     if not args.no_full_mode:
         from paper_2202_07381_b200 import VankaPatchSet
         others = ["full"] if (is3d or is_mhd or conv is not None) \
-            else ["dedup", "kron-sym", "full"]
+            else ["kron", "dedup", "kron-sym", "full"]
         for other in others:
             if other == fine.mode:
                 continue
@@ -619,6 +626,10 @@ def run_ours(args, rank, world, local):
                        "parallelism": f"replicas x{world}"},
             "stage_dof_updates_per_s": world * S.dim / t_step,
             "roofline": {"bound": "hbm", "kernel": f"ivk patch_apply (K2+K3, {fine.mode})",
+                         "limiter": ("modal: 0.22 GB of records per sweep -- issue/latency "
+                                     "bound (ncu: ~0.5 IPC, per-patch dependent phases), not "
+                                     "HBM; kron's HBM-bound K3 is in formulations.kron")
+                         if fine.mode == "modal" else "hbm stream of the inverse store",
                          "achieved": k3_bytes / t_k3 / 1e9, "peak": hbm, "unit": "GB/s",
                          "frac": k3_bytes / t_k3 / 1e9 / hbm,
                          "traffic": measured_traffic(cfg["name"], fine.mode),

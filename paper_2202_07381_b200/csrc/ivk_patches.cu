@@ -1173,6 +1173,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_kernel(
       double acc[NA];
 #pragma unroll
       for (int q = 0; q < NA; ++q) acc[q] = 0.0;
+#pragma unroll 4
       for (int al = 0; al < k; ++al) {
         const double w = W[al * ld + i];
         double rr[NA];
@@ -1254,6 +1255,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_kernel(
 #pragma unroll
       for (int q = 0; q < NA; ++q) acc[q] = 0.0;
       const double* wr = W + al * ld;
+#pragma unroll 4
       for (int i = 0; i < k; ++i) {
         const double w = wr[i];
         double vv[NA];
