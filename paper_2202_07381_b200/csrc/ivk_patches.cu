@@ -1301,6 +1301,296 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_kernel(
   }
 }
 
+// K3m on the FP64 tensor cores (DMMA.8x8x4), for patches with k <= KP nodes:
+// T = W^T R and U = W V as 8x8x4 tiles (M = modes / nodes, N = the NA
+// (component, stage) columns padded to 8, K = nodes / modes), zero padding
+// by predication on the compact record (no extra HBM bytes); everything else
+// as patch_apply_modal_kernel.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__host__ __device__ __forceinline__ int modal_tc_seg(int S, int NC, int kmax, int KP) {
+  const int NW = 8 * ((NC * S + 7) / 8);
+  return (2 * modal_rec(S, NC, kmax) + 2 * KP * NW + 2 * 4 + KP * NW + KP * S * S + 3) & ~3;
+}
+
+template <int S, int NC, int KP>
+__global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
+    PatchParams pd, ModalParams mp, const double* __restrict__ r, double* __restrict__ local,
+    int kmax) {
+  extern __shared__ __align__(16) double modal_sm[];
+  __shared__ __align__(8) uint64_t bars[kApplyWarps][2];
+  constexpr int NA = NC * S;
+  constexpr int NT = (NA + 7) / 8;   // 8-column N tiles
+  constexpr int NW = 8 * NT;         // padded row width of R / T
+  constexpr int MT = KP / 8, KT = KP / 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int gq = lane >> 2, gk = lane & 3;
+  const int recmax = modal_rec(S, NC, kmax);
+  double* buf0 = modal_sm + (long)warp * modal_tc_seg(S, NC, kmax, KP);
+  double* buf1 = buf0 + recmax;
+  double* rsT0 = buf1 + recmax;      // R: [alpha][NW], zero padded rows / columns
+  double* rsT1 = rsT0 + KP * NW;
+  double* rsP = rsT1 + KP * NW;      // the s pressures, two buffers of 4
+  double* t = rsP + 8;               // T / w / v: [i][NW]
+  double* Es = t + KP * NW;
+  for (int e = lane; e < 3 * KP * NW; e += 32) rsT0[e] = 0.0;   // rsT0, rsT1, rsP, t
+  if (lane == 0) {
+    mbar_init(&bars[warp][0], 1);
+    mbar_init(&bars[warp][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const double dt = mp.dt;
+  const int stride = gridDim.x * nw;
+  int p = blockIdx.x * nw + warp;
+  if (lane == 0 && p < pd.num_patches) {
+    const int k0 = pd.node_off[p + 1] - pd.node_off[p];
+    bulk_load(buf0, pd.inv + pd.inv_off[p], modal_rec(S, NC, k0) * 8, &bars[warp][0]);
+  }
+  if (p < pd.num_patches) {
+    const int off0 = pd.idx_off[p];
+    const int k0 = pd.node_off[p + 1] - pd.node_off[p];
+    const int blk0 = NC * k0 + 1;
+    for (int j = lane; j < S * blk0; j += 32) {
+      const int a = (j >= blk0) + (S > 2 && j >= 2 * blk0);
+      const int e = j - a * blk0;
+      const double v = __ldg(r + pd.idx[off0 + j]);
+      if (e < NC * k0) {
+        const int al = e / NC, d = e - al * NC;
+        rsT0[al * NW + d * S + a] = v;
+      } else {
+        rsP[a] = v;
+      }
+    }
+  }
+  uint32_t phase = 0;
+  for (int it = 0; p < pd.num_patches; ++it, p += stride) {
+    const int slot = it & 1;
+    const int pn = p + stride;
+    if (lane == 0 && pn < pd.num_patches) {
+      const int kn = pd.node_off[pn + 1] - pd.node_off[pn];
+      bulk_load(slot ? buf0 : buf1, pd.inv + pd.inv_off[pn], modal_rec(S, NC, kn) * 8,
+                &bars[warp][slot ^ 1]);
+    }
+    const int off = pd.idx_off[p];
+    const int k = pd.node_off[p + 1] - pd.node_off[p];
+    const int blk = NC * k + 1;
+    const int ld = k | 1;
+    const double* R = slot ? rsT1 : rsT0;
+    const double* Rp = rsP + 4 * slot;
+    // next patch: gather indices now, r values after step 1 (m <= 128 prefetched)
+    int pf_idx[4];
+    int pn_off = 0, pn_k = 0, pn_blk = 0;
+    if (pn < pd.num_patches) {
+      pn_off = pd.idx_off[pn];
+      pn_k = pd.node_off[pn + 1] - pd.node_off[pn];
+      pn_blk = NC * pn_k + 1;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = lane + 32 * u;
+      pf_idx[u] = (pn < pd.num_patches && j < S * pn_blk) ? __ldg(pd.idx + pn_off + j) : -1;
+    }
+    mbar_wait(&bars[warp][slot], (phase >> slot) & 1u);
+    phase ^= 1u << slot;
+    __syncwarp();
+    const double* W = slot ? buf1 : buf0;
+    const double* th = W + k * ld;
+    const double* ch = th + k;
+    const double* hi = ch + NC * k;
+    // T = W^T R
+    {
+      double d[MT][NT][2];
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) d[m][n][0] = d[m][n][1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        if (4 * kt < k) {
+          const int al = 4 * kt + gk;
+          double b[NT];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) b[n] = R[al * NW + 8 * n + gq];
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            const int i = 8 * m + gq;
+            const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) dmma884(d[m][n][0], d[m][n][1], a, b[n]);
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          double2 v2 = make_double2(d[m][n][0], d[m][n][1]);
+          *reinterpret_cast<double2*>(t + (8 * m + gq) * NW + 8 * n + 2 * gk) = v2;
+        }
+    }
+    __syncwarp();
+    double pf_val[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) pf_val[u] = pf_idx[u] >= 0 ? __ldg(r + pf_idx[u]) : 0.0;
+    // lane per mode i: w_i = E_i t_i, g += c^ w
+    double g[S];
+#pragma unroll
+    for (int a = 0; a < S; ++a) g[a] = 0.0;
+    for (int i = lane; i < k; i += 32) {
+      double acc[NA];
+      lds_vec<NA>(t + i * NW, acc);
+      double E[S * S];
+      modal_small_inv<S>(mp.a, dt * th[i], E);
+#pragma unroll
+      for (int e = 0; e < S * S; ++e) Es[i * S * S + e] = E[e];
+#pragma unroll
+      for (int dd = 0; dd < NC; ++dd) {
+        const double c = ch[i * NC + dd];
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+          double w = 0.0;
+#pragma unroll
+          for (int b = 0; b < S; ++b) w = fma(E[a * S + b], acc[dd * S + b], w);
+          t[i * NW + dd * S + a] = w;
+          g[a] = fma(c, w, g[a]);
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) g[a] += __shfl_down_sync(0xffffffffu, g[a], o);
+      g[a] = __shfl_sync(0xffffffffu, g[a], 0);
+    }
+    double rhs[S], pv[S], Ap[S];
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+      double s_ = 0.0;
+#pragma unroll
+      for (int b = 0; b < S; ++b) s_ = fma(mp.a[a * S + b], g[b], s_);
+      rhs[a] = dt * s_ - Rp[a];
+    }
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+      double s_ = 0.0;
+#pragma unroll
+      for (int b = 0; b < S; ++b) s_ = fma(hi[a * S + b], rhs[b], s_);
+      pv[a] = s_;
+    }
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+      double s_ = 0.0;
+#pragma unroll
+      for (int b = 0; b < S; ++b) s_ = fma(mp.a[a * S + b], pv[b], s_);
+      Ap[a] = s_;
+    }
+    for (int i = lane; i < k; i += 32) {
+      double e[S];
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        double s_ = 0.0;
+#pragma unroll
+        for (int b = 0; b < S; ++b) s_ = fma(Es[i * S * S + a * S + b], Ap[b], s_);
+        e[a] = s_;
+      }
+#pragma unroll
+      for (int dd = 0; dd < NC; ++dd) {
+        const double c = dt * ch[i * NC + dd];
+#pragma unroll
+        for (int a = 0; a < S; ++a) t[i * NW + dd * S + a] = fma(-c, e[a], t[i * NW + dd * S + a]);
+      }
+    }
+    __syncwarp();
+    // U = W V; each lane writes its two D entries of every tile
+    {
+      double d[MT][NT][2];
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) d[m][n][0] = d[m][n][1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        if (4 * kt < k) {
+          const int i = 4 * kt + gk;
+          double b[NT];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) b[n] = t[i * NW + 8 * n + gq];
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            const int al = 8 * m + gq;
+            const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) dmma884(d[m][n][0], d[m][n][1], a, b[n]);
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int al = 8 * m + gq;
+        if (al < k) {
+#pragma unroll
+          for (int n = 0; n < NT; ++n)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int q = 8 * n + 2 * gk + h;
+              if (q < NA) {
+                const int dd = q / S, a = q - dd * S;
+                const int pos = off + a * blk + NC * al + dd;
+                st_keep(local + (pd.slot_pos ? pd.slot_pos[pos] : pos), d[m][n][h]);
+              }
+            }
+        }
+      }
+    }
+    if (lane < S) {
+      const int pos = off + lane * blk + NC * k;
+      double pl = pv[0];
+#pragma unroll
+      for (int a = 1; a < S; ++a)
+        if (lane == a) pl = pv[a];
+      st_keep(local + (pd.slot_pos ? pd.slot_pos[pos] : pos), pl);
+    }
+    __syncwarp();
+    // land the next patch's r values; clear the rows a previous (larger)
+    // patch left behind, so the tensor-core tiles read zeros past k
+    {
+      double* RN = slot ? rsT0 : rsT1;
+      double* RPN = rsP + 4 * (slot ^ 1);
+      for (int e = pn_k * NW + lane; e < KP * NW; e += 32) RN[e] = 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = lane + 32 * u;
+        if (pf_idx[u] >= 0) {
+          const int a = (j >= pn_blk) + (S > 2 && j >= 2 * pn_blk);
+          const int e = j - a * pn_blk;
+          if (e < NC * pn_k) {
+            const int al = e / NC, dd = e - al * NC;
+            RN[al * NW + dd * S + a] = pf_val[u];
+          } else {
+            RPN[a] = pf_val[u];
+          }
+        }
+      }
+      for (int j = 128 + lane; pn < pd.num_patches && j < S * pn_blk; j += 32) {
+        const int a = (j >= pn_blk) + (S > 2 && j >= 2 * pn_blk);
+        const int e = j - a * pn_blk;
+        const double v = __ldg(r + pd.idx[pn_off + j]);
+        if (e < NC * pn_k) {
+          const int al = e / NC, dd = e - al * NC;
+          RN[al * NW + dd * S + a] = v;
+        } else {
+          RPN[a] = v;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------------- K7g (general path)
 //
 // One CTA per patch of a general stage operator I_s (x) M + dt A (x) L
@@ -2102,14 +2392,20 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
     mp.dt = md->dt;
     for (int i = 0; i < IVK_MAX_STAGES * IVK_MAX_STAGES; ++i) mp.a[i] = md->butcher_a[i];
     const int kmax = (pd->max_m / md->stages - 1) / md->ncomp;
-    const size_t seg = (size_t)modal_seg(mp.S, mp.NC, kmax) * sizeof(double);
-    // warps per CTA: three CTAs per SM when the per-warp buffers allow it
-    int nw = (int)((72 * 1024) / seg);
-    if (nw > kApplyWarps) nw = kApplyWarps;
-    if (nw < 1) nw = 1;
-    IVK_REQUIRE(seg <= 200 * 1024, "modal patch (k = %d) exceeds shared memory", kmax);
-    const size_t smem = seg * nw;
+    size_t seg = (size_t)modal_seg(mp.S, mp.NC, kmax) * sizeof(double);
     void (*fn)(PatchParams, ModalParams, const double*, double*, int) = nullptr;
+    size_t seg_tc = 0;
+    if (kmax <= 32) {
+      // FP64 tensor-core variant (K padded to 24 or 32 node slots)
+      const int KP = kmax <= 24 ? 24 : 32;
+      seg_tc = (size_t)modal_tc_seg(mp.S, mp.NC, kmax, KP) * sizeof(double);
+#define IVK_TC(SS, CC)                                                                       \
+  if (mp.S == SS && mp.NC == CC)                                                             \
+    fn = KP == 24 ? patch_apply_modal_tc_kernel<SS, CC, 24> : patch_apply_modal_tc_kernel<SS, CC, 32>;
+      IVK_TC(1, 2) IVK_TC(2, 2) IVK_TC(3, 2) IVK_TC(1, 3) IVK_TC(2, 3) IVK_TC(3, 3)
+#undef IVK_TC
+    }
+    if (fn == nullptr) {
     if (mp.NC == 2) {
       if (mp.S == 1) fn = patch_apply_modal_kernel<1, 2>;
       else if (mp.S == 2) fn = patch_apply_modal_kernel<2, 2>;
@@ -2119,6 +2415,15 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       else if (mp.S == 2) fn = patch_apply_modal_kernel<2, 3>;
       else fn = patch_apply_modal_kernel<3, 3>;
     }
+    } else {
+      seg = seg_tc;
+    }
+    // warps per CTA: three CTAs per SM when the per-warp buffers allow it
+    int nw = (int)((72 * 1024) / seg);
+    if (nw > kApplyWarps) nw = kApplyWarps;
+    if (nw < 1) nw = 1;
+    IVK_REQUIRE(seg <= 200 * 1024, "modal patch (k = %d) exceeds shared memory", kmax);
+    const size_t smem = seg * nw;
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) {

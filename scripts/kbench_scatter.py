@@ -17,8 +17,7 @@ from paper_2202_07381_b200._device import ptr, stream  # noqa: E402
 def main(name, mode):
     cfg = bench.CONFIGS[name]
     disc, tab, conv = bench.make_disc(cfg)
-    mg, S = disc.build_mg(tab, cfg["dt"], SmootherSpec(), convection=conv, patch_mode=mode,
-                          mg_levels=2)
+    mg, S = disc.build_mg(tab, cfg["dt"], SmootherSpec(), convection=conv, patch_mode=mode)
     b = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, S.dim)).cuda()
     L = _lib.lib()
     for scatter in ("patch", "owner"):
