@@ -364,10 +364,10 @@ def run_ours(args, rank, world, local):
     t0 = time.perf_counter()
     # the headline sweep runs a per-patch formulation valid on any mesh:
     # "modal" (Stokes: per-patch generalised eigenbasis, modal.py) on the 2-D
-    # Stokes configs, "kron" (Butcher eigen-split blocks) where a convection or
-    # a general multi-field operator breaks the M_s (x) I / K_s (x) I structure
-    # and for 3-D (its modal kernel is not tuned yet)
-    head = "modal" if (conv is None and not is3d and not is_mhd) else "kron"
+    # and 3-D Stokes configs, "kron" (Butcher eigen-split blocks) where a
+    # convection or a general multi-field operator breaks the M_s (x) I /
+    # K_s (x) I structure
+    head = "modal" if (conv is None and not is_mhd) else "kron"
     mg, S = disc.build_mg(tab, cfg["dt"], cheb, convection=conv, patch_mode=head)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
@@ -504,8 +504,8 @@ def run_ours(args, rank, world, local):
                                 "inverse_bytes": 8 * fine.inv_size}}
     if not args.no_full_mode:
         from paper_2202_07381_b200 import VankaPatchSet
-        others = ["full"] if (is3d or is_mhd or conv is not None) \
-            else ["kron", "dedup", "kron-sym", "full"]
+        others = (["kron", "full"] if is3d else ["full"] if (is_mhd or conv is not None)
+                  else ["kron", "dedup", "kron-sym", "full"])
         for other in others:
             if other == fine.mode:
                 continue

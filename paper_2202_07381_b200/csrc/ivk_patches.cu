@@ -1591,6 +1591,280 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
   }
 }
 
+// K3m for large patches (3-D: k = 65 nodes, W_s 34 KB): one CTA of
+// kModalCtaWarps warps per patch (persistent over patches, 2 CTAs per SM), the
+// record double-buffered by TMA bulk copies, the two GEMMs on the FP64 tensor cores
+// with the 8-row tiles split over the warps, the per-mode work thread per
+// mode, the pressure Schur solve by thread 0 after a fixed-order CTA reduction.
+constexpr int kModalCtaWarps = 16;
+
+__host__ __device__ __forceinline__ int modal_cta_smem(int S, int NC, int kmax, int KP) {
+  const int NW = 8 * ((NC * S + 7) / 8);
+  return (2 * modal_rec(S, NC, kmax) + 2 * KP * NW + 8 + KP * NW + KP * S * S +
+          kModalCtaWarps * 4 + 8 + 3) & ~3;
+}
+
+template <int S, int NC, int KP>
+__global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_kernel(
+    PatchParams pd, ModalParams mp, const double* __restrict__ r, double* __restrict__ local,
+    int kmax) {
+  extern __shared__ __align__(16) double modal_sm[];
+  __shared__ __align__(8) uint64_t bars[2];
+  constexpr int NA = NC * S;
+  constexpr int NT = (NA + 7) / 8;
+  constexpr int NW = 8 * NT;
+  constexpr int MT = KP / 8, KT = KP / 4;
+  constexpr int NTH = kModalCtaWarps * 32;
+  constexpr int PF = 4;             // prefetched r values per thread (m <= 512)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, gk = lane & 3;
+  const int recmax = modal_rec(S, NC, kmax);
+  double* buf0 = modal_sm;
+  double* buf1 = buf0 + recmax;
+  double* R0 = buf1 + recmax;
+  double* R1 = R0 + KP * NW;
+  double* Rp = R1 + KP * NW;        // 2 x 4 pressures
+  double* t = Rp + 8;
+  double* Es = t + KP * NW;
+  double* gred = Es + KP * S * S;   // kModalCtaWarps x 4 partial sums
+  double* pAp = gred + kModalCtaWarps * 4;  // p (4) and A p (4)
+  for (int e = tid; e < 2 * KP * NW + 8 + KP * NW; e += NTH) R0[e] = 0.0;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double dt = mp.dt;
+  int p = blockIdx.x;
+  if (tid == 0 && p < pd.num_patches) {
+    const int k0 = pd.node_off[p + 1] - pd.node_off[p];
+    bulk_load(buf0, pd.inv + pd.inv_off[p], modal_rec(S, NC, k0) * 8, &bars[0]);
+  }
+  if (p < pd.num_patches) {
+    const int off0 = pd.idx_off[p];
+    const int k0 = pd.node_off[p + 1] - pd.node_off[p];
+    const int blk0 = NC * k0 + 1;
+    for (int j = tid; j < S * blk0; j += NTH) {
+      const int a = (j >= blk0) + (S > 2 && j >= 2 * blk0);
+      const int e = j - a * blk0;
+      const double v = __ldg(r + pd.idx[off0 + j]);
+      if (e < NC * k0) {
+        const int al = e / NC, d = e - al * NC;
+        R0[al * NW + d * S + a] = v;
+      } else {
+        Rp[a] = v;
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int it = 0; p < pd.num_patches; ++it, p += gridDim.x) {
+    const int slot = it & 1;
+    const int pn = p + gridDim.x;
+    if (tid == 0 && pn < pd.num_patches) {
+      const int kn = pd.node_off[pn + 1] - pd.node_off[pn];
+      bulk_load(slot ? buf0 : buf1, pd.inv + pd.inv_off[pn], modal_rec(S, NC, kn) * 8,
+                &bars[slot ^ 1]);
+    }
+    const int off = pd.idx_off[p];
+    const int k = pd.node_off[p + 1] - pd.node_off[p];
+    const int blk = NC * k + 1;
+    const int ld = k | 1;
+    const double* R = slot ? R1 : R0;
+    const double* Rpc = Rp + 4 * slot;
+    int pf_idx[PF];
+    int pn_off = 0, pn_k = 0, pn_blk = 0;
+    if (pn < pd.num_patches) {
+      pn_off = pd.idx_off[pn];
+      pn_k = pd.node_off[pn + 1] - pd.node_off[pn];
+      pn_blk = NC * pn_k + 1;
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int j = tid + NTH * u;
+      pf_idx[u] = (pn < pd.num_patches && j < S * pn_blk) ? __ldg(pd.idx + pn_off + j) : -1;
+    }
+    mbar_wait(&bars[slot], (phase >> slot) & 1u);
+    phase ^= 1u << slot;
+    const double* W = slot ? buf1 : buf0;
+    const double* th = W + k * ld;
+    const double* ch = th + k;
+    const double* hi = ch + NC * k;
+    // T = W^T R: warp w takes mode tiles w, w + 4, ...
+    for (int m = warp; m < MT; m += kModalCtaWarps) {
+      if (8 * m >= k) break;
+      double d[NT][2];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) d[n][0] = d[n][1] = 0.0;
+      const int i = 8 * m + gq;
+#pragma unroll 4
+      for (int kt = 0; kt < KT; ++kt) {
+        if (4 * kt >= k) break;
+        const int al = 4 * kt + gk;
+        const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) dmma884(d[n][0], d[n][1], a, R[al * NW + 8 * n + gq]);
+      }
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+        *reinterpret_cast<double2*>(t + i * NW + 8 * n + 2 * gk) = make_double2(d[n][0], d[n][1]);
+    }
+    double pf_val[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) pf_val[u] = pf_idx[u] >= 0 ? __ldg(r + pf_idx[u]) : 0.0;
+    __syncthreads();
+    // thread per mode: w_i = E_i t_i, g += c^ w
+    double g[S];
+#pragma unroll
+    for (int a = 0; a < S; ++a) g[a] = 0.0;
+    for (int i = tid; i < k; i += NTH) {
+      double acc[NA];
+      lds_vec<NA>(t + i * NW, acc);
+      double E[S * S];
+      modal_small_inv<S>(mp.a, dt * th[i], E);
+#pragma unroll
+      for (int e = 0; e < S * S; ++e) Es[i * S * S + e] = E[e];
+#pragma unroll
+      for (int dd = 0; dd < NC; ++dd) {
+        const double c = ch[i * NC + dd];
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+          double w = 0.0;
+#pragma unroll
+          for (int b = 0; b < S; ++b) w = fma(E[a * S + b], acc[dd * S + b], w);
+          t[i * NW + dd * S + a] = w;
+          g[a] = fma(c, w, g[a]);
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) g[a] += __shfl_down_sync(0xffffffffu, g[a], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int a = 0; a < S; ++a) gred[warp * 4 + a] = g[a];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double gg[S], rhs[S], pv[S];
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        gg[a] = gred[a];
+        for (int w = 1; w < kModalCtaWarps; ++w) gg[a] += gred[w * 4 + a];
+      }
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        double s_ = 0.0;
+#pragma unroll
+        for (int b = 0; b < S; ++b) s_ = fma(mp.a[a * S + b], gg[b], s_);
+        rhs[a] = dt * s_ - Rpc[a];
+      }
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        double s_ = 0.0;
+#pragma unroll
+        for (int b = 0; b < S; ++b) s_ = fma(hi[a * S + b], rhs[b], s_);
+        pv[a] = s_;
+        pAp[a] = s_;
+      }
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        double s_ = 0.0;
+#pragma unroll
+        for (int b = 0; b < S; ++b) s_ = fma(mp.a[a * S + b], pv[b], s_);
+        pAp[4 + a] = s_;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < k; i += NTH) {
+      double e[S];
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        double s_ = 0.0;
+#pragma unroll
+        for (int b = 0; b < S; ++b) s_ = fma(Es[i * S * S + a * S + b], pAp[4 + b], s_);
+        e[a] = s_;
+      }
+#pragma unroll
+      for (int dd = 0; dd < NC; ++dd) {
+        const double c = dt * ch[i * NC + dd];
+#pragma unroll
+        for (int a = 0; a < S; ++a) t[i * NW + dd * S + a] = fma(-c, e[a], t[i * NW + dd * S + a]);
+      }
+    }
+    __syncthreads();
+    // U = W V: warp w takes node tiles w, w + 4, ...
+    for (int m = warp; m < MT; m += kModalCtaWarps) {
+      if (8 * m >= k) break;
+      double d[NT][2];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) d[n][0] = d[n][1] = 0.0;
+      const int al = 8 * m + gq;
+#pragma unroll 4
+      for (int kt = 0; kt < KT; ++kt) {
+        if (4 * kt >= k) break;
+        const int i = 4 * kt + gk;
+        const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) dmma884(d[n][0], d[n][1], a, t[i * NW + 8 * n + gq]);
+      }
+      if (al < k) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int q = 8 * n + 2 * gk + h;
+            if (q < NA) {
+              const int dd = q / S, a = q - dd * S;
+              const int pos = off + a * blk + NC * al + dd;
+              st_keep(local + (pd.slot_pos ? pd.slot_pos[pos] : pos), d[n][h]);
+            }
+          }
+      }
+    }
+    if (tid < S) {
+      const int pos = off + tid * blk + NC * k;
+      st_keep(local + (pd.slot_pos ? pd.slot_pos[pos] : pos), pAp[tid]);
+    }
+    // clear t rows this patch wrote (the next patch may be smaller) and land
+    // the next patch's r
+    {
+      double* RN = slot ? R0 : R1;
+      double* RPN = Rp + 4 * (slot ^ 1);
+      for (int e = pn_k * NW + tid; e < KP * NW; e += NTH) RN[e] = 0.0;
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int j = tid + NTH * u;
+        if (pf_idx[u] >= 0) {
+          const int a = (j >= pn_blk) + (S > 2 && j >= 2 * pn_blk);
+          const int e = j - a * pn_blk;
+          if (e < NC * pn_k) {
+            const int al = e / NC, dd = e - al * NC;
+            RN[al * NW + dd * S + a] = pf_val[u];
+          } else {
+            RPN[a] = pf_val[u];
+          }
+        }
+      }
+      for (int j = PF * NTH + tid; pn < pd.num_patches && j < S * pn_blk; j += NTH) {
+        const int a = (j >= pn_blk) + (S > 2 && j >= 2 * pn_blk);
+        const int e = j - a * pn_blk;
+        const double v = __ldg(r + pd.idx[pn_off + j]);
+        if (e < NC * pn_k) {
+          const int al = e / NC, dd = e - al * NC;
+          RN[al * NW + dd * S + a] = v;
+        } else {
+          RPN[a] = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------- K7g (general path)
 //
 // One CTA per patch of a general stage operator I_s (x) M + dt A (x) L
@@ -2404,6 +2678,28 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
     fn = KP == 24 ? patch_apply_modal_tc_kernel<SS, CC, 24> : patch_apply_modal_tc_kernel<SS, CC, 32>;
       IVK_TC(1, 2) IVK_TC(2, 2) IVK_TC(3, 2) IVK_TC(1, 3) IVK_TC(2, 3) IVK_TC(3, 3)
 #undef IVK_TC
+    }
+    if (fn == nullptr && kmax <= 72) {
+      // large (3-D: k = 65) patches: CTA per patch, 4 warps sharing the tiles
+      const size_t smem = (size_t)modal_cta_smem(mp.S, mp.NC, kmax, 72) * sizeof(double);
+      IVK_REQUIRE(smem <= 200 * 1024, "modal patch (k = %d) exceeds shared memory", kmax);
+#define IVK_CTA(SS, CC) \
+  if (mp.S == SS && mp.NC == CC) fn = patch_apply_modal_cta_kernel<SS, CC, 72>;
+      IVK_CTA(1, 2) IVK_CTA(2, 2) IVK_CTA(3, 2) IVK_CTA(1, 3) IVK_CTA(2, 3) IVK_CTA(3, 3)
+#undef IVK_CTA
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) {
+          set_error("ivk_patch_apply: %s", cudaGetErrorString(e));
+          return IVK_ECUDA;
+        }
+      }
+      const int per_sm = (int)((226 * 1024) / (smem + 1024));
+      int cgrid = kSMs * (per_sm < 1 ? 1 : per_sm);
+      if (cgrid > pd->num_patches) cgrid = pd->num_patches;
+      fn<<<cgrid, kModalCtaWarps * 32, smem, st>>>(p, mp, r, local, kmax);
+      return check_launch("ivk_patch_apply(modal, cta)");
     }
     if (fn == nullptr) {
     if (mp.NC == 2) {
