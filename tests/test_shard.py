@@ -176,7 +176,8 @@ def test_sharded_sweep_two_ranks_gloo(monkeypatch):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,nparts,mode", [("s3", 2, "auto"), ("s3", 3, "kron"),
-                                              ("ns", 4, "auto"), ("crossed", 2, "full")])
+                                              ("ns", 4, "auto"), ("crossed", 2, "full"),
+                                              ("s3", 2, "modal"), ("crossed", 3, "modal")])
 def test_sharded_sweep_device_loopback(name, nparts, mode):
     import torch
     from paper_2202_07381_b200 import VankaPatchSet, apply_vanka
