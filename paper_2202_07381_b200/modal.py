@@ -105,11 +105,12 @@ class ModalSplit:
             E = torch.linalg.inv(eye + dt * theta[..., None, None] * A)        # (P, k, s, s)
             wsum = torch.einsum("pi,piab->pab", (chat * chat).sum(-1), E)
             H = dt * dt * (A @ wsum @ A)
-            Hinv = torch.linalg.inv(H)
+            Hinv, hinfo = torch.linalg.inv_ex(H)
             # 1-norm condition number (exact for the s x s Schur complement;
             # an SVD per patch would cost more than the factorisation)
             cond = torch.linalg.matrix_norm(H, ord=1) * torch.linalg.matrix_norm(Hinv, ord=1)
-            ok = (info == 0) & torch.isfinite(Hinv).flatten(1).all(1) & (cond < 1e14)
+            ok = (info == 0) & (hinfo == 0) & torch.isfinite(Hinv).flatten(1).all(1) & \
+                (cond < 1e14)
             rec = self.record_doubles(int(k))
             body = self._pack(W, theta, chat, Hinv, torch)
             off = int(patches.inv_off[first])

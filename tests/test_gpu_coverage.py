@@ -88,7 +88,7 @@ def test_singular_patch_detected():
     tab = tableau_lookup("backwardeuler", 1)
     # dt = 0: the patch pressure rows vanish -> every patch matrix is singular
     S = StageSystem(disc.blocks[0], tab, 0.0, disc.cdofs[0])
-    for mode in ("full", "kron"):
+    for mode in ("full", "kron", "modal"):
         with pytest.raises(PatchSingularError) as ei:
             VankaPatchSet(S, disc.hier.levels[0], mode=mode)
         assert 0 <= ei.value.vertex < disc.hier.levels[0].num_vertices
