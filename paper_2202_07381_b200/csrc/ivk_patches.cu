@@ -973,14 +973,6 @@ struct ModalParams {
 __host__ __device__ __forceinline__ int modal_rec(int S, int NC, int k) {
   return (k * (k | 1) + k + NC * k + S * S + 3) & ~3;
 }
-// per warp: two record buffers (double-buffered bulk copies), two r_p buffers
-// (the next patch's gather is prefetched), t, E
-__host__ __device__ __forceinline__ int modal_seg(int S, int NC, int kmax) {
-  const int NA = NC * S;
-  return (2 * modal_rec(S, NC, kmax) + 2 * ((kmax * NA + S + 1) & ~1) + kmax * NA +
-          kmax * S * S + 3) & ~3;  // 32-byte aligned (TMA destinations, 16-byte smem vector loads)
-}
-
 template <int NC>
 __global__ void __launch_bounds__(128) patch_gather_blocks_kernel(FactorParams op, PatchParams pd,
                                                                   int kmax, double* __restrict__ Ms,
@@ -1068,239 +1060,6 @@ __device__ __forceinline__ void lds_vec(const double* p, double (&v)[N]) {
   }
 }
 
-template <int S, int NC>
-__global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_kernel(
-    PatchParams pd, ModalParams mp, const double* __restrict__ r, double* __restrict__ local,
-    int kmax) {
-  extern __shared__ __align__(16) double modal_sm[];
-  __shared__ __align__(8) uint64_t bars[kApplyWarps][2];
-  constexpr int NA = NC * S;  // (component, stage) pairs per mode / node
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int recmax = modal_rec(S, NC, kmax);
-  double* buf0 = modal_sm + (long)warp * modal_seg(S, NC, kmax);
-  double* buf1 = buf0 + recmax;
-  const int rsn = (kmax * NA + S + 1) & ~1;
-  double* rsT0 = buf1 + recmax;                // r_p: [alpha][d][a], then the s pressures
-  double* rsT1 = rsT0 + rsn;                   // (double-buffered: next patch prefetched)
-  double* t = rsT1 + rsn;                      // W^T r, then w, then v: [i][d][a]
-  double* Es = t + kmax * NA;                  // E_i = (I + dt theta_i A)^-1
-  if (lane == 0) {
-    mbar_init(&bars[warp][0], 1);
-    mbar_init(&bars[warp][1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  double A[S * S];
-#pragma unroll
-  for (int e = 0; e < S * S; ++e) A[e] = mp.a[e];
-  const double dt = mp.dt;
-  const int stride = gridDim.x * nw;
-  int p = blockIdx.x * nw + warp;
-  // one TMA bulk copy per patch record, one record ahead of the compute
-  if (lane == 0 && p < pd.num_patches) {
-    const int k0 = pd.node_off[p + 1] - pd.node_off[p];
-    bulk_load(buf0, pd.inv + pd.inv_off[p], modal_rec(S, NC, k0) * 8, &bars[warp][0]);
-  }
-  if (p < pd.num_patches) {
-    const int off0 = pd.idx_off[p];
-    const int k0 = pd.node_off[p + 1] - pd.node_off[p];
-    const int blk0 = NC * k0 + 1;
-    for (int j = lane; j < S * blk0 && j < 128; j += 32) {
-      const int a = (j >= blk0) + (S > 2 && j >= 2 * blk0);
-      const int e = j - a * blk0;
-      const double v = __ldg(r + pd.idx[off0 + j]);
-      if (e < NC * k0) {
-        const int al = e / NC, d = e - al * NC;
-        rsT0[al * NA + d * S + a] = v;
-      } else {
-        rsT0[k0 * NA + a] = v;
-      }
-    }
-  }
-  uint32_t phase = 0;
-  for (int it = 0; p < pd.num_patches; ++it, p += stride) {
-    const int slot = it & 1;
-    const int pn = p + stride;
-    if (lane == 0 && pn < pd.num_patches) {
-      const int kn = pd.node_off[pn + 1] - pd.node_off[pn];
-      bulk_load(slot ? buf0 : buf1, pd.inv + pd.inv_off[pn], modal_rec(S, NC, kn) * 8,
-                &bars[warp][slot ^ 1]);
-    }
-    const int off = pd.idx_off[p];
-    const int k = pd.node_off[p + 1] - pd.node_off[p];
-    const int blk = NC * k + 1;
-    const int ld = k | 1;
-    // r_p: the first 128 entries were prefetched into registers during the
-    // previous patch (pf); the rest (3-D patches) are gathered here
-    double* rsT = slot ? rsT1 : rsT0;
-    for (int j = 128 + lane; j < S * blk; j += 32) {
-      const int a = (j >= blk) + (S > 2 && j >= 2 * blk);
-      const int e = j - a * blk;
-      const double v = __ldg(r + pd.idx[off + j]);
-      if (e < NC * k) {
-        const int al = e / NC, d = e - al * NC;
-        rsT[al * NA + d * S + a] = v;
-      } else {
-        rsT[k * NA + a] = v;
-      }
-    }
-    // next patch: its gather indices now, its r values after step 1
-    int pf_idx[4];
-    int pn_off = 0, pn_k = 0, pn_blk = 0;
-    if (pn < pd.num_patches) {
-      pn_off = pd.idx_off[pn];
-      pn_k = pd.node_off[pn + 1] - pd.node_off[pn];
-      pn_blk = NC * pn_k + 1;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = lane + 32 * u;
-      pf_idx[u] = (pn < pd.num_patches && j < S * pn_blk) ? __ldg(pd.idx + pn_off + j) : -1;
-    }
-    mbar_wait(&bars[warp][slot], (phase >> slot) & 1u);
-    phase ^= 1u << slot;
-    __syncwarp();
-    const double* W = slot ? buf1 : buf0;
-    const double* th = W + k * ld;
-    const double* ch = th + k;
-    const double* hi = ch + NC * k;
-    // lane per mode i: t_i = W^T r for every (d, a) at once, w_i = E_i t_i,
-    // g += c^ w
-    double g[S];
-#pragma unroll
-    for (int a = 0; a < S; ++a) g[a] = 0.0;
-    for (int i = lane; i < k; i += 32) {
-      double acc[NA];
-#pragma unroll
-      for (int q = 0; q < NA; ++q) acc[q] = 0.0;
-#pragma unroll 4
-      for (int al = 0; al < k; ++al) {
-        const double w = W[al * ld + i];
-        double rr[NA];
-        lds_vec<NA>(rsT + al * NA, rr);
-#pragma unroll
-        for (int q = 0; q < NA; ++q) acc[q] = fma(w, rr[q], acc[q]);
-      }
-      double E[S * S];
-      modal_small_inv<S>(A, dt * th[i], E);
-#pragma unroll
-      for (int e = 0; e < S * S; ++e) Es[i * S * S + e] = E[e];
-#pragma unroll
-      for (int d = 0; d < NC; ++d) {
-        const double c = ch[i * NC + d];
-#pragma unroll
-        for (int a = 0; a < S; ++a) {
-          double w = 0.0;
-#pragma unroll
-          for (int b = 0; b < S; ++b) w = fma(E[a * S + b], acc[d * S + b], w);
-          t[i * NA + d * S + a] = w;
-          g[a] = fma(c, w, g[a]);
-        }
-      }
-    }
-    double pf_val[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) pf_val[u] = pf_idx[u] >= 0 ? __ldg(r + pf_idx[u]) : 0.0;
-    // fixed-order tree to lane 0, then broadcast (every lane the same bits)
-#pragma unroll
-    for (int a = 0; a < S; ++a) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) g[a] += __shfl_down_sync(0xffffffffu, g[a], o);
-      g[a] = __shfl_sync(0xffffffffu, g[a], 0);
-    }
-    // p = H^-1 (dt A g - q),  Ap = A p
-    double rhs[S], pv[S], Ap[S];
-#pragma unroll
-    for (int a = 0; a < S; ++a) {
-      double s_ = 0.0;
-#pragma unroll
-      for (int b = 0; b < S; ++b) s_ = fma(A[a * S + b], g[b], s_);
-      rhs[a] = dt * s_ - rsT[k * NA + a];
-    }
-#pragma unroll
-    for (int a = 0; a < S; ++a) {
-      double s_ = 0.0;
-#pragma unroll
-      for (int b = 0; b < S; ++b) s_ = fma(hi[a * S + b], rhs[b], s_);
-      pv[a] = s_;
-    }
-#pragma unroll
-    for (int a = 0; a < S; ++a) {
-      double s_ = 0.0;
-#pragma unroll
-      for (int b = 0; b < S; ++b) s_ = fma(A[a * S + b], pv[b], s_);
-      Ap[a] = s_;
-    }
-    // v_i = w_i - dt c^ E_i A p  (each lane rewrites its own modes)
-    for (int i = lane; i < k; i += 32) {
-      double e[S];
-#pragma unroll
-      for (int a = 0; a < S; ++a) {
-        double s_ = 0.0;
-#pragma unroll
-        for (int b = 0; b < S; ++b) s_ = fma(Es[i * S * S + a * S + b], Ap[b], s_);
-        e[a] = s_;
-      }
-#pragma unroll
-      for (int d = 0; d < NC; ++d) {
-        const double c = dt * ch[i * NC + d];
-#pragma unroll
-        for (int a = 0; a < S; ++a) t[i * NA + d * S + a] = fma(-c, e[a], t[i * NA + d * S + a]);
-      }
-    }
-    __syncwarp();
-    // lane per node alpha: u[a][NC alpha + d] = sum_i W[alpha][i] v[i][d][a]
-    for (int al = lane; al < k; al += 32) {
-      double acc[NA];
-#pragma unroll
-      for (int q = 0; q < NA; ++q) acc[q] = 0.0;
-      const double* wr = W + al * ld;
-#pragma unroll 4
-      for (int i = 0; i < k; ++i) {
-        const double w = wr[i];
-        double vv[NA];
-        lds_vec<NA>(t + i * NA, vv);
-#pragma unroll
-        for (int q = 0; q < NA; ++q) acc[q] = fma(w, vv[q], acc[q]);
-      }
-#pragma unroll
-      for (int d = 0; d < NC; ++d)
-#pragma unroll
-        for (int a = 0; a < S; ++a) {
-          const int pos = off + a * blk + NC * al + d;
-          st_keep(local + (pd.slot_pos ? pd.slot_pos[pos] : pos), acc[d * S + a]);
-        }
-    }
-    if (lane < S) {
-      const int pos = off + lane * blk + NC * k;
-      double pl = pv[0];
-#pragma unroll
-      for (int a = 1; a < S; ++a)
-        if (lane == a) pl = pv[a];
-      st_keep(local + (pd.slot_pos ? pd.slot_pos[pos] : pos), pl);
-    }
-    // land the next patch's prefetched r values
-    {
-      double* rsN = slot ? rsT0 : rsT1;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = lane + 32 * u;
-        if (pf_idx[u] >= 0) {
-          const int a = (j >= pn_blk) + (S > 2 && j >= 2 * pn_blk);
-          const int e = j - a * pn_blk;
-          if (e < NC * pn_k) {
-            const int al = e / NC, d = e - al * NC;
-            rsN[al * NA + d * S + a] = pf_val[u];
-          } else {
-            rsN[pn_k * NA + a] = pf_val[u];
-          }
-        }
-      }
-    }
-    __syncwarp();
-  }
-}
-
 // K3m on the FP64 tensor cores (DMMA.8x8x4), for patches with k <= KP nodes:
 // T = W^T R and U = W V as 8x8x4 tiles (M = modes / nodes, N = the NA
 // (component, stage) columns padded to 8, K = nodes / modes), zero padding
@@ -1344,13 +1103,18 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
   }
   __syncwarp();
   const double dt = mp.dt;
-  const int stride = gridDim.x * nw;
-  int p = blockIdx.x * nw + warp;
-  if (lane == 0 && p < pd.num_patches) {
+  // each CTA walks a contiguous run of patches (neighbouring vertex stars:
+  // their r gathers and local[] writes share cache lines), warps interleaved
+  const int stride = nw;
+  const int chunk = (pd.num_patches + gridDim.x - 1) / gridDim.x;
+  const int pbeg = blockIdx.x * chunk;
+  const int pend = min(pd.num_patches, pbeg + chunk);
+  int p = pbeg + warp;
+  if (lane == 0 && p < pend) {
     const int k0 = pd.node_off[p + 1] - pd.node_off[p];
     bulk_load(buf0, pd.inv + pd.inv_off[p], modal_rec(S, NC, k0) * 8, &bars[warp][0]);
   }
-  if (p < pd.num_patches) {
+  if (p < pend) {
     const int off0 = pd.idx_off[p];
     const int k0 = pd.node_off[p + 1] - pd.node_off[p];
     const int blk0 = NC * k0 + 1;
@@ -1367,10 +1131,10 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
     }
   }
   uint32_t phase = 0;
-  for (int it = 0; p < pd.num_patches; ++it, p += stride) {
+  for (int it = 0; p < pend; ++it, p += stride) {
     const int slot = it & 1;
     const int pn = p + stride;
-    if (lane == 0 && pn < pd.num_patches) {
+    if (lane == 0 && pn < pend) {
       const int kn = pd.node_off[pn + 1] - pd.node_off[pn];
       bulk_load(slot ? buf0 : buf1, pd.inv + pd.inv_off[pn], modal_rec(S, NC, kn) * 8,
                 &bars[warp][slot ^ 1]);
@@ -1384,7 +1148,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
     // next patch: gather indices now, r values after step 1 (m <= 128 prefetched)
     int pf_idx[4];
     int pn_off = 0, pn_k = 0, pn_blk = 0;
-    if (pn < pd.num_patches) {
+    if (pn < pend) {
       pn_off = pd.idx_off[pn];
       pn_k = pd.node_off[pn + 1] - pd.node_off[pn];
       pn_blk = NC * pn_k + 1;
@@ -1392,7 +1156,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int j = lane + 32 * u;
-      pf_idx[u] = (pn < pd.num_patches && j < S * pn_blk) ? __ldg(pd.idx + pn_off + j) : -1;
+      pf_idx[u] = (pn < pend && j < S * pn_blk) ? __ldg(pd.idx + pn_off + j) : -1;
     }
     mbar_wait(&bars[warp][slot], (phase >> slot) & 1u);
     phase ^= 1u << slot;
@@ -1575,7 +1339,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
           }
         }
       }
-      for (int j = 128 + lane; pn < pd.num_patches && j < S * pn_blk; j += 32) {
+      for (int j = 128 + lane; pn < pend && j < S * pn_blk; j += 32) {
         const int a = (j >= pn_blk) + (S > 2 && j >= 2 * pn_blk);
         const int e = j - a * pn_blk;
         const double v = __ldg(r + pd.idx[pn_off + j]);
@@ -2666,7 +2430,7 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
     mp.dt = md->dt;
     for (int i = 0; i < IVK_MAX_STAGES * IVK_MAX_STAGES; ++i) mp.a[i] = md->butcher_a[i];
     const int kmax = (pd->max_m / md->stages - 1) / md->ncomp;
-    size_t seg = (size_t)modal_seg(mp.S, mp.NC, kmax) * sizeof(double);
+    size_t seg = 0;
     void (*fn)(PatchParams, ModalParams, const double*, double*, int) = nullptr;
     size_t seg_tc = 0;
     if (kmax <= 32) {
@@ -2680,7 +2444,7 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
 #undef IVK_TC
     }
     if (fn == nullptr && kmax <= 72) {
-      // large (3-D: k = 65) patches: CTA per patch, 4 warps sharing the tiles
+      // large (3-D: k = 65) patches: CTA per patch, its warps sharing the tiles
       const size_t smem = (size_t)modal_cta_smem(mp.S, mp.NC, kmax, 72) * sizeof(double);
       IVK_REQUIRE(smem <= 200 * 1024, "modal patch (k = %d) exceeds shared memory", kmax);
 #define IVK_CTA(SS, CC) \
@@ -2702,18 +2466,10 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       return check_launch("ivk_patch_apply(modal, cta)");
     }
     if (fn == nullptr) {
-    if (mp.NC == 2) {
-      if (mp.S == 1) fn = patch_apply_modal_kernel<1, 2>;
-      else if (mp.S == 2) fn = patch_apply_modal_kernel<2, 2>;
-      else fn = patch_apply_modal_kernel<3, 2>;
-    } else {
-      if (mp.S == 1) fn = patch_apply_modal_kernel<1, 3>;
-      else if (mp.S == 2) fn = patch_apply_modal_kernel<2, 3>;
-      else fn = patch_apply_modal_kernel<3, 3>;
+      set_error("ivk_patch_apply: modal patches with k = %d > 72 nodes unsupported", kmax);
+      return IVK_EUNSUPPORTED;
     }
-    } else {
-      seg = seg_tc;
-    }
+    seg = seg_tc;
     // warps per CTA: three CTAs per SM when the per-warp buffers allow it
     int nw = (int)((72 * 1024) / seg);
     if (nw > kApplyWarps) nw = kApplyWarps;

@@ -247,6 +247,8 @@ class VankaPatchSet:
             # Stokes only: velocity blocks M_s (x) I and K_s (x) I, K_s symmetric
             if self.general or system.convection is not None:
                 raise ValueError("modal split needs a convection-free Taylor-Hood operator")
+            if int(np.diff(self.tables.node_off).max()) > 72:
+                raise ValueError("modal split supports patches of at most 72 free nodes")
             from .modal import ModalSplit
             self.modal = ModalSplit(system.tableau, system.dt, system.nc)
         # kron-sym halves the inverse bytes but measures no faster than kron on
