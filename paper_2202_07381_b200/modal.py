@@ -23,6 +23,28 @@ from . import _lib
 __all__ = ["ModalSplit"]
 
 
+def _bitwise_classes(rows):
+    """(rep, inverse): indices of one representative per class of bitwise
+    identical rows and each row's class.  A 64-bit multiplicative hash of the
+    bit patterns groups rows; every row is then compared with its class
+    representative and any mismatch (a hash collision) becomes its own class."""
+    import torch
+    bits = rows.contiguous().view(torch.int64)
+    g = torch.Generator(device="cpu").manual_seed(12345)
+    mult = (torch.randint(1, 2 ** 62, (bits.shape[1],), generator=g, dtype=torch.int64) | 1)
+    h = (bits * mult.to(bits.device)).sum(dim=1)
+    _, first_inv = torch.unique(h, return_inverse=True)
+    n = len(h)
+    order = torch.arange(n, device=h.device)
+    first = torch.full((int(first_inv.max()) + 1,), n, dtype=torch.int64, device=h.device)
+    first = first.scatter_reduce(0, first_inv, order, reduce="amin")
+    cand = first[first_inv]
+    same = (bits == bits[cand]).all(dim=1)
+    cls = torch.where(same, cand, order)                    # colliding rows stand alone
+    rep, inverse = torch.unique(cls, return_inverse=True)
+    return rep, inverse
+
+
 class ModalSplit:
     def __init__(self, tableau, dt, ncomp):
         self.A = np.asarray(tableau.A, dtype=np.float64)
@@ -92,15 +114,21 @@ class ModalSplit:
             Mk = Ms[first:first + count, :k, :k]
             Kk = Ks[first:first + count, :k, :k]
             Ck = Cb[first:first + count, :k, :]
-            L, info = torch.linalg.cholesky_ex(Mk)
-            X = torch.linalg.solve_triangular(L, Kk, upper=False)              # L^-1 K
+            # the eigenbasis depends on (M_s, K_s) only: patches whose blocks are
+            # bitwise identical (translation-invariant stars) share one
+            # decomposition -- found by a hash, then confirmed bit for bit
+            rep, inv = _bitwise_classes(torch.cat([Mk.reshape(count, -1),
+                                                   Kk.reshape(count, -1)], dim=1))
+            L, info = torch.linalg.cholesky_ex(Mk[rep])
+            X = torch.linalg.solve_triangular(L, Kk[rep], upper=False)         # L^-1 K
             Cm = torch.linalg.solve_triangular(L, X.mT, upper=False)           # L^-1 K L^-T
             Cm = 0.5 * (Cm + Cm.mT)
             # cuSOLVER's batched eigensolver takes bounded batches
-            parts = [torch.linalg.eigh(Cm[i:i + 4096]) for i in range(0, count, 4096)]
-            theta = torch.cat([q[0] for q in parts])
+            parts = [torch.linalg.eigh(Cm[i:i + 4096]) for i in range(0, len(rep), 4096)]
+            theta = torch.cat([q[0] for q in parts])[inv]
             Q = torch.cat([q[1] for q in parts])
-            W = torch.linalg.solve_triangular(L.mT, Q, upper=True)             # L^-T Q
+            W = torch.linalg.solve_triangular(L.mT, Q, upper=True)[inv]       # L^-T Q
+            info = info[inv]
             chat = W.mT @ Ck                                                   # (P, k, nc)
             E = torch.linalg.inv(eye + dt * theta[..., None, None] * A)        # (P, k, s, s)
             wsum = torch.einsum("pi,piab->pab", (chat * chat).sum(-1), E)
