@@ -125,3 +125,24 @@ def test_replicas_two_ranks_gloo():
     assert all(r[1] == 2 for r in res)
     assert all(r[2] == 2.0 for r in res)          # max over ranks
     assert res[0][3] == res[1][3]                # replicas agree bitwise
+
+
+def test_patch_mode_validation_on_host():
+    """Formulation choices are validated before any device work (CPU): the
+    modal split needs a convection-free Taylor-Hood operator, kron-sym / dedup
+    a symmetric translation-invariant one, general operators run kron / full."""
+    from paper_2202_07381_b200 import VankaPatchSet, tableau_lookup
+    from paper_2202_07381_b200.mhd import MHDDiscretization
+    from harness import setup
+    disc, tab, conv, case = setup("ns")
+    from paper_2202_07381_b200.stages import assemble_stage_operator
+    S = assemble_stage_operator(disc.blocks[-1], tab, case["dt"], constrained=disc.cdofs[-1],
+                                convection=conv[-1])
+    for mode in ("modal", "kron-sym", "dedup", "bogus"):
+        with pytest.raises(ValueError):
+            VankaPatchSet(S, disc.fine_mesh, mode=mode, factor=False)
+    md = MHDDiscretization(4, 1)
+    G = md.system(1, tableau_lookup("radauiia", 2), 0.01)
+    for mode in ("modal", "kron-sym", "dedup"):
+        with pytest.raises(ValueError):
+            VankaPatchSet(G, md.fine_mesh, mode=mode, factor=False)
