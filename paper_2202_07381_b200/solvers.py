@@ -337,8 +337,16 @@ class VankaPatchSet:
 
     @property
     def patch_vel(self):
+        """Per-vertex P2 (velocity; for general operators every P2 field)
+        single-stage DoFs of each patch (solvers.py:160)."""
         t = self.tables
         out = [None] * t.num_patches
+        if self.general:
+            nw = self.system.nc * self.system.n_nodes
+            for k, v in enumerate(t.order):
+                d = t.node[t.node_off[k]:t.node_off[k + 1]]
+                out[v] = d[d < nw].astype(np.int64)
+            return out
         for k, v in enumerate(t.order):
             n = t.node[t.node_off[k]:t.node_off[k + 1]]
             vel = np.empty(2 * len(n), dtype=np.int64)

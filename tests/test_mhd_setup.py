@@ -133,3 +133,19 @@ def test_mhd_configs_are_baseline_shaped():
     c = MHD_CONFIGS["cfg5"]
     assert (c["n0"] * 2 ** c["level"], c["stages"], c["dt"], c["seed"]) == (128, 2, 1 / 128, 4)
     assert tableau_lookup(c["family"], c["stages"]).r == 2
+
+
+def test_patch_vel_general_lists_p2_dofs():
+    """VankaPatchSet.patch_vel on a general system: the P2 (u, B) DoFs of each
+    star, consistent with the stage-0 part of patch_indices (host tables only)."""
+    from paper_2202_07381_b200.general import build_general_patch_tables
+    disc, tab, case = mhd_setup("mhd16")
+    S = disc.system(disc.num_levels - 1, tab, case["dt"])
+    t = build_general_patch_tables(disc.fine_mesh, S)
+    nw = S.nc * S.n_nodes
+    for k in range(0, t.num_patches, 37):
+        single = t.node[t.node_off[k]:t.node_off[k + 1]]
+        idx = t.idx[t.idx_off[k]:t.idx_off[k + 1]]
+        assert np.array_equal(idx[:len(single)], single)
+        w = single[single < nw]
+        assert len(single) - len(w) in (1, 2)        # p (and r unless on the boundary)
