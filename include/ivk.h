@@ -284,6 +284,24 @@ int ivk_index_update(int64_t n, const int32_t* idx, double alpha, const double* 
 int ivk_patch_gather_blocks(const ivk_operator_desc* op, const ivk_patch_desc* pd, int32_t kmax,
                             double* Ms, double* Ks, double* C, void* stream);
 
+/* Sharded sweep over peer memory: the partial-sum
+ * exchange + ordered reduction + x update of a strip-sharded sweep fused into
+ * one kernel that reads the other ranks' patch outputs directly (NVLink P2P
+ * loads through mapped peer pointers; in-process shards in tests).  For
+ * own DoF d = dofs[i]: z = sum over the ranks holding d (holder_rank[
+ * holder_ptr[i] .. holder_ptr[i+1]), ascending) of sum_k local_q[dof_pos_q[k]],
+ * k in [dof_ptr_q[d], dof_ptr_q[d+1]); x[d] += omega * w[d] * z.  Every rank
+ * holding d adds the same terms in the same order: the same bits. */
+typedef struct ivk_peer_view {
+  const int32_t* dof_ptr;  /* that rank's patch-set tables (global DoF index) */
+  const int32_t* dof_pos;
+  const double* local;     /* that rank's patch outputs (K3)                  */
+} ivk_peer_view;
+
+int ivk_peer_combine_update(int32_t n, const int32_t* dofs, const int32_t* holder_ptr,
+                            const int32_t* holder_rank, const ivk_peer_view* peers_dev,
+                            double omega, const double* w, double* x, void* stream);
+
 /* Assemble every patch matrix from the operator (solvers.py:186-212) and
  * invert it in place into pd->inv (np.linalg.inv, solvers.py:177) by
  * Gauss-Jordan with partial pivoting.  *singular_dev (device int32, set to

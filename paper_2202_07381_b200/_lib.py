@@ -114,6 +114,10 @@ class CoarseDesc(C.Structure):
     ]
 
 
+class PeerView(C.Structure):
+    _fields_ = [("dof_ptr", C.c_void_p), ("dof_pos", C.c_void_p), ("local", C.c_void_p)]
+
+
 class GeneralDesc(C.Structure):
     _fields_ = [
         ("stages", C.c_int32), ("n", C.c_int32), ("nnz", C.c_int32), ("dt", C.c_double),
@@ -186,6 +190,7 @@ _SIGS = {
     "ivk_lincomb": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P], C.c_int),
     "ivk_patch_gather_blocks": ([C.POINTER(OperatorDesc), C.POINTER(PatchDesc), C.c_int32, _P,
                                  _P, _P, _P], C.c_int),
+    "ivk_peer_combine_update": ([C.c_int32, _P, _P, _P, _P, C.c_double, _P, _P, _P], C.c_int),
     "ivk_general_apply": ([C.POINTER(GeneralDesc), _P, _P, _P, _P], C.c_int),
     "ivk_general_patch_factor": ([C.POINTER(GeneralDesc), C.POINTER(PatchDesc), _P, _P], C.c_int),
     "ivk_general_vanka_sweep": ([C.POINTER(GeneralDesc), C.POINTER(PatchDesc), _P, _P, C.c_double,

@@ -200,6 +200,26 @@ __global__ void patch_combine_kernel(PatchParams pd, const double* __restrict__ 
   }
 }
 
+// K4p: the sharded sweep's exchange + ordered reduction + update in one
+// kernel over peer memory (ivk_peer_combine_update).
+__global__ void peer_combine_update_kernel(int n, const int32_t* __restrict__ dofs,
+                                           const int32_t* __restrict__ holder_ptr,
+                                           const int32_t* __restrict__ holder_rank,
+                                           const ivk_peer_view* __restrict__ peers,
+                                           double omega, const double* __restrict__ w,
+                                           double* __restrict__ x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int d = dofs[i];
+    double z = 0.0;
+    for (int h = holder_ptr[i]; h < holder_ptr[i + 1]; ++h) {
+      const ivk_peer_view pv = peers[holder_rank[h]];
+      const int k0 = pv.dof_ptr[d], k1 = pv.dof_ptr[d + 1];
+      for (int k = k0; k < k1; ++k) z += pv.local[pv.dof_pos[k]];
+    }
+    x[d] = fma(omega * (w ? w[d] : 1.0), z, x[d]);
+  }
+}
+
 // -------------------------------------------------------------------- K7
 
 struct FactorParams {
@@ -2722,6 +2742,19 @@ int ivk_patch_gather_blocks(const ivk_operator_desc* op, const ivk_patch_desc* p
   else
     patch_gather_blocks_kernel<2><<<pd->num_patches, 128, 0, as_stream(stream)>>>(f, p, kmax, Ms, Ks, C);
   return check_launch("ivk_patch_gather_blocks");
+}
+
+int ivk_peer_combine_update(int32_t n, const int32_t* dofs, const int32_t* holder_ptr,
+                            const int32_t* holder_rank, const ivk_peer_view* peers_dev,
+                            double omega, const double* w, double* x, void* stream) {
+  IVK_REQUIRE(n >= 0 && dofs && holder_ptr && holder_rank && peers_dev && x,
+              "bad peer combine arguments");
+  if (n == 0) return IVK_OK;
+  int grid = (n + 255) / 256;
+  if (grid > kSMs * 16) grid = kSMs * 16;
+  peer_combine_update_kernel<<<grid, 256, 0, as_stream(stream)>>>(n, dofs, holder_ptr, holder_rank,
+                                                                  peers_dev, omega, w, x);
+  return check_launch("ivk_peer_combine_update");
 }
 
 int ivk_general_patch_factor(const ivk_general_desc* op, const ivk_patch_desc* pd,

@@ -39,7 +39,7 @@ import numpy as np
 from .patches import _ranges, build_patch_tables
 
 __all__ = ["StripPartition", "ShardPlan", "shard_plans", "ShardedSweep", "DeviceBackend",
-           "DistComm", "LoopbackGroup"]
+           "DistComm", "LoopbackGroup", "PeerShard", "PeerLoopback", "SymmetricPeers"]
 
 
 class StripPartition:
@@ -305,3 +305,140 @@ class LoopbackGroup:
         for s, x in zip(self.shards, xs):
             s.halo(x)
         return xs
+
+
+# ------------------------------------------------- fused exchange over peers
+
+class PeerShard:
+    """One rank's sweep with the exchange fused into the update kernel
+    (``ivk_peer_combine_update``): after K1 + K3 on its patches, the rank sums
+    every own DoF's contributions from ALL ranks holding it -- reading their
+    patch outputs through peer pointers (NVLink P2P loads) in ascending rank
+    order -- and updates x, then pulls its halo straight from the owners' x.
+    No packed buffers, no send/recv: 2 kernels + 1 copy kernel per provider.
+
+    The peer table (``set_peers``) maps rank -> (dof_ptr, dof_pos, local, x)
+    device pointers: in-process shards in tests (``PeerLoopback``), symmetric
+    memory mapped over NVLink across processes (``SymmetricPeers``)."""
+
+    def __init__(self, plan, backend, omega=0.5, local=None):
+        import torch
+        from ._device import upload
+        self.plan = plan
+        self.be = backend
+        self.omega = float(omega)
+        self.r = backend.empty(backend.dim)
+        dev = backend.patches.device_data()
+        self.local = dev["local"] if local is None else local
+        self.dof_ptr, self.dof_pos = dev["dof_ptr"], dev["dof_pos"]
+        holders = [[plan.rank] for _ in plan.dofs]
+        pos = {int(d): i for i, d in enumerate(plan.dofs)}
+        for q, dd in plan.shared.items():
+            for d in dd:
+                holders[pos[int(d)]].append(q)
+        hp = np.concatenate([[0], np.cumsum([len(h) for h in holders])])
+        hr = np.concatenate([sorted(h) for h in holders]) if len(holders) else np.zeros(0)
+        self.holder_ptr = upload(hp, np.int32)
+        self.holder_rank = upload(hr, np.int32)
+        self.dofs = backend.dofs
+        self.hr = {q: backend.index(s_) for q, s_ in plan.halo_recv.items()}
+        self.peers_dev = None
+        self.peer_x = {}
+        self._torch = torch
+
+    def view(self):
+        """(dof_ptr, dof_pos, local) device pointers of this rank."""
+        return (self.dof_ptr.data_ptr(), self.dof_pos.data_ptr(), self.local.data_ptr())
+
+    def set_peers(self, views, x_ptrs):
+        """views[q] = (dof_ptr, dof_pos, local) and x_ptrs[q] = x of rank q, as
+        device addresses valid on this rank."""
+        tbl = np.asarray(views, dtype=np.uint64).reshape(-1, 3).view(np.int64)
+        self.peers_dev = self._torch.from_numpy(tbl.copy()).cuda()
+        self.peer_x = dict(enumerate(x_ptrs))
+
+    def local_phase(self, x, b):
+        self.be.residual(x, b, self.r)
+        self.be.patches.apply_local(self.r, self.local)
+
+    def combine_phase(self, x):
+        from ._device import ptr, stream
+        from . import _lib
+        _lib.check(_lib.lib().ivk_peer_combine_update(
+            len(self.plan.dofs), ptr(self.dofs), ptr(self.holder_ptr), ptr(self.holder_rank),
+            ptr(self.peers_dev), self.omega, ptr(self.be.w), ptr(x), stream()),
+            "peer_combine_update")
+
+    def halo_phase(self, x):
+        from ._device import ptr, stream
+        from . import _lib
+        for q, idx in self.hr.items():
+            # x[idx] = x_q[idx]: a gather over NVLink from the owner's iterate
+            _lib.check(_lib.lib().ivk_index_copy(len(idx), ptr(idx), self.peer_x[q], ptr(idx),
+                                                 ptr(x), 0.0, stream()), "index_copy(peer)")
+
+
+class PeerLoopback:
+    """All ranks' shards in one process (the 1-GPU emulation of the peer
+    path: every phase runs for all shards before the next phase, so no kernel
+    ever waits on another)."""
+
+    def __init__(self, shards, xs):
+        self.shards = shards
+        views = [s.view() for s in shards]
+        x_ptrs = [x.data_ptr() for x in xs]
+        for s in shards:
+            s.set_peers(views, x_ptrs)
+
+    def sweep(self, xs, b):
+        for s, x in zip(self.shards, xs):
+            s.local_phase(x, b)
+        for s, x in zip(self.shards, xs):
+            s.combine_phase(x)
+        for s, x in zip(self.shards, xs):
+            s.halo_phase(x)
+        return xs
+
+
+class SymmetricPeers:
+    """Multi-process wiring of ``PeerShard`` (one rank per GPU): the patch
+    outputs, DoF tables and iterate live in torch symmetric memory, whose
+    rendezvous maps every peer's buffer into this rank's address space over
+    NVLink; the phases are separated by process-group barriers (host-side:
+    no kernel waits on another rank).  Not exercised here -- the environment
+    has one GPU; the kernel and the phase logic are the ones PeerLoopback
+    tests."""
+
+    def __init__(self, plan, backend, x, omega=0.5, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.group = group if group is not None else dist.group.WORLD
+        dev = backend.patches.device_data()
+        world = dist.get_world_size(self.group)
+
+        def symmetric(src):
+            n = torch.tensor([src.numel()], device=src.device)
+            dist.all_reduce(n, op=dist.ReduceOp.MAX, group=self.group)
+            t = symm.empty(int(n.item()), dtype=src.dtype, device=src.device)
+            t[:src.numel()].copy_(src)
+            return t, symm.rendezvous(t, self.group)
+
+        self.local, hl = symmetric(dev["local"])
+        self.dof_ptr, hp = symmetric(dev["dof_ptr"])
+        self.dof_pos, hq = symmetric(dev["dof_pos"])
+        self.x, hx = symmetric(x)
+        self.shard = PeerShard(plan, backend, omega, local=self.local[:dev["local"].numel()])
+        views = [(hp.buffer_ptrs[q], hq.buffer_ptrs[q], hl.buffer_ptrs[q]) for q in range(world)]
+        self.shard.set_peers(views, [hx.buffer_ptrs[q] for q in range(world)])
+
+    def sweep(self, b):
+        import torch.distributed as dist
+        x = self.x[:self.shard.be.dim]
+        self.shard.local_phase(x, b)
+        dist.barrier(group=self.group)
+        self.shard.combine_phase(x)
+        dist.barrier(group=self.group)
+        self.shard.halo_phase(x)
+        dist.barrier(group=self.group)
+        return x

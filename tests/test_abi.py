@@ -48,6 +48,7 @@ STRUCTS = {
     "ivk_general_desc": _lib.GeneralDesc,
     "ivk_general_transfer_desc": _lib.GeneralTransferDesc,
     "ivk_modal_desc": _lib.ModalDesc,
+    "ivk_peer_view": _lib.PeerView,
 }
 
 
