@@ -39,7 +39,8 @@ import numpy as np
 from .patches import _ranges, build_patch_tables
 
 __all__ = ["StripPartition", "ShardPlan", "shard_plans", "ShardedSweep", "DeviceBackend",
-           "DistComm", "LoopbackGroup", "PeerShard", "PeerLoopback", "SymmetricPeers"]
+           "DistComm", "LoopbackGroup", "PeerShard", "PeerLoopback", "SymmetricPeers",
+           "peer_holders"]
 
 
 class StripPartition:
@@ -309,6 +310,21 @@ class LoopbackGroup:
 
 # ------------------------------------------------- fused exchange over peers
 
+def peer_holders(plan):
+    """CSR (ptr, ranks) over the plan's own DoFs: the ranks whose patches
+    contain each DoF, ascending (the fused kernel's summation order)."""
+    n = len(plan.dofs)
+    cols = [np.full(n, plan.rank, dtype=np.int64)]
+    rows = [np.arange(n)]
+    for q, dd in plan.shared.items():
+        cols.append(np.full(len(dd), q, dtype=np.int64))
+        rows.append(np.searchsorted(plan.dofs, dd))
+    rows, cols = np.concatenate(rows), np.concatenate(cols)
+    order = np.lexsort((cols, rows))
+    ptr = np.concatenate([[0], np.cumsum(np.bincount(rows, minlength=n))])
+    return ptr.astype(np.int64), cols[order]
+
+
 class PeerShard:
     """One rank's sweep with the exchange fused into the update kernel
     (``ivk_peer_combine_update``): after K1 + K3 on its patches, the rank sums
@@ -331,13 +347,7 @@ class PeerShard:
         dev = backend.patches.device_data()
         self.local = dev["local"] if local is None else local
         self.dof_ptr, self.dof_pos = dev["dof_ptr"], dev["dof_pos"]
-        holders = [[plan.rank] for _ in plan.dofs]
-        pos = {int(d): i for i, d in enumerate(plan.dofs)}
-        for q, dd in plan.shared.items():
-            for d in dd:
-                holders[pos[int(d)]].append(q)
-        hp = np.concatenate([[0], np.cumsum([len(h) for h in holders])])
-        hr = np.concatenate([sorted(h) for h in holders]) if len(holders) else np.zeros(0)
+        hp, hr = peer_holders(plan)
         self.holder_ptr = upload(hp, np.int32)
         self.holder_rank = upload(hr, np.int32)
         self.dofs = backend.dofs

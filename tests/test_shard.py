@@ -253,3 +253,24 @@ def test_peer_fused_sweep_loopback(name, nparts, mode):
         for q, s in p.shared.items():
             idx = torch.from_numpy(s).cuda()
             assert torch.equal(x[idx], xs[q][idx])
+
+
+def test_peer_holders_cover_every_contribution():
+    """CPU: the fused kernel's holder lists name, for every own DoF, exactly
+    the ranks whose patches contain it, ascending; summed over ranks the
+    holder counts reproduce the global patch multiplicity's support."""
+    from paper_2202_07381_b200.patches import build_patch_tables
+    from paper_2202_07381_b200.shard import StripPartition, peer_holders, shard_plans
+    disc, tab, conv, case, S, mesh = _problem("s3")
+    plans = shard_plans(S, mesh, StripPartition(mesh, 3))
+    t = build_patch_tables(mesh, S.n_nodes, S.n_p, S.r, S.node_constrained)
+    part = StripPartition(mesh, 3).part
+    owner_of_entry = np.repeat(part[t.order], t.sizes)
+    for p in plans:
+        ptr, ranks = peer_holders(p)
+        assert len(ptr) == len(p.dofs) + 1
+        for i in range(0, len(p.dofs), 97):
+            d = p.dofs[i]
+            expect = np.unique(owner_of_entry[t.idx == d])
+            got = ranks[ptr[i]:ptr[i + 1]]
+            assert np.array_equal(got, expect) and p.rank in got
