@@ -216,9 +216,11 @@ class VankaPatchSet:
     symmetric tile-triangle (Stokes: no convection; 44% fewer bytes than
     kron at cfg2); "dedup" shares the kron blocks of patches whose
     canonical matrices are bitwise identical (translation-invariant
-    operators: dedup.py); "auto" picks dedup when it collapses the patch
-    set at least 8x (convection-free), else kron (all stages share the
-    convection Jacobian, A well diagonalisable, b <= 64), else full.
+    operators: dedup.py); "modal" the per-patch generalised eigenbasis of
+    the Stokes velocity blocks (modal.py: ~10x fewer bytes than kron, any
+    tableau); "auto" picks dedup when it collapses the patch set at least 8x
+    (2-D, convection-free), else modal (convection-free), else kron (all
+    stages share the convection Jacobian, A well diagonalisable), else full.
     """
 
     def __init__(self, system, mesh, omega=1.0, factor=True, mode="auto", scatter="patch",
@@ -292,6 +294,13 @@ class VankaPatchSet:
             dd = build_dedup_tables(mesh, system, self.tables)
             if mode == "dedup" or dd.n_classes * 8 <= self.tables.num_patches:
                 self.dedup = dd
+        if (mode == "auto" and self.dedup is None and not self.general and
+                system.convection is None and int(np.diff(self.tables.node_off).max()) <= 72):
+            # convection-free Taylor-Hood operator on a mesh without enough
+            # repeated patches: the modal split (any tableau, fewest bytes)
+            from .modal import ModalSplit
+            self.kron = None
+            self.modal = ModalSplit(system.tableau, system.dt, system.nc)
         self.mode = "modal" if self.modal is not None else "full" if self.kron is None else \
             ("dedup" if self.dedup is not None else
              ("kron-sym" if self.kron.symmetric else "kron"))

@@ -37,7 +37,7 @@ class Case:
         self.mg, self.S = self.disc.build_mg(self.tab, c["dt"], cheb, convection=self.conv,
                                              patch_mode=mode)
         expect = mode if mode != "auto" else \
-            ("kron" if c["conv"] or name == "crossed" else "dedup")
+            ("kron" if c["conv"] else "modal" if name == "crossed" else "dedup")
         assert self.mg.levels[-1].patches.mode == expect
         pou = SmootherSpec(pre=2, post=2, accel="richardson", omega=0.5, weighting="pou")
         self.mg_pou = MGHierarchyOp([MGLevel(l.system, l.patches, pou, l.prolong)
