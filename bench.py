@@ -465,6 +465,36 @@ def run_ours(args, rank, world, local):
         for h in (mg, mg_pou):
             h._graph = None
 
+    # One full IRK Newton step of Navier-Stokes on the device (newton.py,
+    # SURVEY.md §8(f) #3): per-stage J_N on every level (K10), K7 refactor,
+    # FGMRES + V-cycle per Newton iteration, u_n = the config's advecting field
+    newton = None
+    if conv is not None and not args.no_full_mode:
+        try:
+            from paper_2202_07381_b200 import fem as _fem
+            from paper_2202_07381_b200.discretization import streamfunction_velocity
+            from paper_2202_07381_b200.newton import NewtonConfig, NSStageNewton
+            u_n = _fem.interpolate_velocity(disc.fine_mesh, streamfunction_velocity)
+            p_n = np.zeros(disc.fine_mesh.num_vertices)
+            t0 = time.perf_counter()
+            nsn = NSStageNewton(disc, tab, cfg["dt"], cheb)
+            torch.cuda.synchronize()
+            t_build_n = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            _, nst = nsn.solve(u_n, p_n, config=NewtonConfig(atol=1e-8))
+            torch.cuda.synchronize()
+            newton = {"seconds": time.perf_counter() - t0, "setup_s": t_build_n,
+                      "newton_iterations": nst.iterations,
+                      "linear_iterations": [l.iterations for l in nst.linear_stats],
+                      "residual_norms": nst.residual_norms,
+                      "what": "one Gauss(2) stage solve of Navier-Stokes (Re=100) from u_n = "
+                              "the cfg3 advecting field: device residual, per-stage J_N(us_i) "
+                              "on every level (K10), K7 full refactor, FGMRES + V-cycle"}
+            del nsn
+            torch.cuda.empty_cache()
+        except Exception as e:  # reported, never fatal for the headline line
+            newton = {"error": f"{type(e).__name__}: {e}"}
+
     # Full FGMRES solve (device), both smoothers
     def time_solve(h):
         fgmres(S.matvec, b, precond=h.precondition, rtol=1e-8, maxiter=2, restart=50)  # warm
@@ -651,6 +681,7 @@ def run_ours(args, rank, world, local):
             "vcycle_ms": vc,
             "fgmres": solves,
             "dedup_cycle": dedup,
+            "newton_step": newton,
             "sharded": sharded,
             "setup_s": {"discretization": t_disc, "build_mg_gpu_factor": t_build,
                         "newton_relinearize": relin},

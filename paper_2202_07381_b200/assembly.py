@@ -70,6 +70,10 @@ class ConvectionAssembler:
 
     def device_data(self, sell_pos=None):
         if self._dev is not None:
+            if sell_pos is not None and "sell_pos" not in self._dev["tensors"]:
+                from ._device import upload
+                self._dev["tensors"]["sell_pos"] = upload(sell_pos, np.int32)
+                self._dev["desc"].sell_pos = self._dev["tensors"]["sell_pos"].data_ptr()
             return self._dev
         import torch
         from ._device import upload
@@ -131,3 +135,20 @@ class ConvectionAssembler:
                                                       ptr(dev["tensors"]["scratch"]),
                                                       ptr(t["conv"]), ptr(t["conv_s"]), None,
                                                       stream()), "convection_assemble")
+
+    def assemble_stage(self, system, stage, u):
+        """Overwrite stage ``stage``'s device Jacobian of a system carrying one
+        convection Jacobian per stage (n_conv = s, stages.py:118-123)."""
+        from ._device import ptr, stream
+        sdev = system.device_data()
+        if system._conv_vals is None or len(system._conv_vals) != system.r:
+            raise ValueError("system needs one convection Jacobian per stage")
+        if not 0 <= stage < system.r:
+            raise ValueError("stage out of range")
+        dev = self.device_data(sell_pos=system.sell_pos())
+        t = sdev["tensors"]
+        conv, conv_s = t["conv"], t["conv_s"]
+        _lib.check(_lib.lib().ivk_convection_assemble(
+            dev["desc"], ptr(u), ptr(dev["tensors"]["scratch"]),
+            conv[stage].data_ptr(), conv_s[stage].data_ptr(), None, stream()),
+            "convection_assemble")

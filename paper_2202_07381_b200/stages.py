@@ -323,13 +323,15 @@ class StageSystem:
         return sptr[rows // C_] + ent * C_ + rows % C_
 
     def download_convection(self):
-        """Refresh the host copy of the (single, shared) device convection."""
+        """Refresh the host copy of the device convection (one shared Jacobian
+        or one per stage)."""
         if self._dev is None or "conv" not in self._dev["tensors"]:
             return
-        v = self._dev["tensors"]["conv"].reshape(-1, 2, 2).cpu().numpy()
-        self._conv_vals = [v]
-        J = ConvectionBlocks(self.n_nodes, self.blocks.rowptr, self.blocks.col, v)
-        self.convection = [J] * self.r
+        conv = self._dev["tensors"]["conv"]
+        vals = [conv[i].reshape(-1, 2, 2).cpu().numpy() for i in range(conv.shape[0])]
+        self._conv_vals = vals
+        Js = [ConvectionBlocks(self.n_nodes, self.blocks.rowptr, self.blocks.col, v) for v in vals]
+        self.convection = Js * self.r if len(Js) == 1 else Js
 
     @property
     def desc(self):
