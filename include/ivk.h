@@ -424,6 +424,31 @@ typedef struct ivk_general_transfer_desc {
   const uint8_t* coarse_constrained; /* nc                                  */
 } ivk_general_transfer_desc;
 
+/* Device re-linearisation of the 2-D resistive MHD operator (mhd.py, K10g):
+ * the element matrices of L at a new frozen state (u0, B0: (n_nodes, 2) nodal
+ * P2 values each), one thread per (cell, element row), at the degree-5
+ * triangle rule; then every CSR entry sums its (cell, row, column)
+ * contributions in cell order (deterministic) into the l half of op->ml and,
+ * through sell_pos, of op->sml.  The mass half is state-independent. */
+#define IVK_MHD_MAX_QUAD 16
+typedef struct ivk_mhd_desc {
+  int32_t n_cells, nnz, nq;
+  double Re, Rm, S;
+  double w[IVK_MHD_MAX_QUAD];
+  double phi[IVK_MHD_MAX_QUAD * 6];       /* [q][a]                          */
+  double dphi[IVK_MHD_MAX_QUAD * 12];     /* [q][a][e] reference gradients   */
+  double psi[IVK_MHD_MAX_QUAD * 3];       /* [q][v]                          */
+  double dpsi[6];                         /* [v][e]                          */
+  const double* cell_geo;      /* C x 5: Jinv row-major [e][d], det J        */
+  const int32_t* cell_nodes;   /* C x 6 scalar P2 nodes                      */
+  const int32_t* entry_ptr;    /* nnz + 1                                    */
+  const int32_t* entry_contrib;/* cell * 900 + i * 30 + j, cell-ascending    */
+  const int32_t* sell_pos;     /* nnz: SELL-32 position of each CSR entry    */
+} ivk_mhd_desc;
+
+int ivk_mhd_assemble(const ivk_mhd_desc* d, const double* u0, const double* B0,
+                     double* elem_scratch, double* ml, double* sml, void* stream);
+
 /* out = b - A x (b != NULL) or A x; out may alias b.  K1g. */
 int ivk_general_apply(const ivk_general_desc* op, const double* x, const double* b, double* out,
                       void* stream);

@@ -157,6 +157,20 @@ class ConvectionDesc(C.Structure):
     ]
 
 
+class MHDDesc(C.Structure):
+    _fields_ = [
+        ("n_cells", C.c_int32), ("nnz", C.c_int32), ("nq", C.c_int32),
+        ("Re", C.c_double), ("Rm", C.c_double), ("S", C.c_double),
+        ("w", C.c_double * IVK_MAX_QUAD),
+        ("phi", C.c_double * (IVK_MAX_QUAD * 6)),
+        ("dphi", C.c_double * (IVK_MAX_QUAD * 12)),
+        ("psi", C.c_double * (IVK_MAX_QUAD * 3)),
+        ("dpsi", C.c_double * 6),
+        ("cell_geo", C.c_void_p), ("cell_nodes", C.c_void_p),
+        ("entry_ptr", C.c_void_p), ("entry_contrib", C.c_void_p), ("sell_pos", C.c_void_p),
+    ]
+
+
 # name -> argtypes (restype int unless noted)
 _P = C.c_void_p
 _SIGS = {
@@ -191,6 +205,7 @@ _SIGS = {
     "ivk_patch_gather_blocks": ([C.POINTER(OperatorDesc), C.POINTER(PatchDesc), C.c_int32, _P,
                                  _P, _P, _P], C.c_int),
     "ivk_peer_combine_update": ([C.c_int32, _P, _P, _P, _P, C.c_double, _P, _P, _P], C.c_int),
+    "ivk_mhd_assemble": ([C.POINTER(MHDDesc), _P, _P, _P, _P, _P, _P], C.c_int),
     "ivk_general_apply": ([C.POINTER(GeneralDesc), _P, _P, _P, _P], C.c_int),
     "ivk_general_patch_factor": ([C.POINTER(GeneralDesc), C.POINTER(PatchDesc), _P, _P], C.c_int),
     "ivk_general_vanka_sweep": ([C.POINTER(GeneralDesc), C.POINTER(PatchDesc), _P, _P, C.c_double,

@@ -207,6 +207,145 @@ static GenTransferParams make_transfer(const ivk_general_transfer_desc* d) {
   return t;
 }
 
+// ---------------------------------------------------------------- K10g
+// Element rows of the linearised MHD operator (mhd.py element_matrices, the
+// weak form of PAPER.md "MHD semi-discrete"): thread (cell, local row i).
+// Local order: w = 4 a + comp (comp 0, 1: u_x, u_y; 2, 3: B_x, B_y), then
+// r at the 3 vertices (24..26), p at the 3 vertices (27..29).
+struct MhdTables {
+  int nq;
+  double Re, Rm, S;
+  double w[IVK_MHD_MAX_QUAD];
+  double phi[IVK_MHD_MAX_QUAD * 6];
+  double dphi[IVK_MHD_MAX_QUAD * 12];
+  double psi[IVK_MHD_MAX_QUAD * 3];
+  double dpsi[6];
+};
+
+__global__ void mhd_element_kernel(MhdTables tb, int n_cells, const double* __restrict__ geo,
+                                   const int32_t* __restrict__ cnodes,
+                                   const double* __restrict__ u0, const double* __restrict__ B0,
+                                   double* __restrict__ Le) {
+  const long tid = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (tid >= (long)n_cells * 30) return;
+  const int cell = (int)(tid / 30), i = (int)(tid - (long)cell * 30);
+  const double* gg = geo + (long)cell * 5;
+  const double J00 = gg[0], J01 = gg[1], J10 = gg[2], J11 = gg[3], det = gg[4];
+  int nd[6];
+  double u0n[6][2], B0n[6][2];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    nd[a] = cnodes[(long)cell * 6 + a];
+    u0n[a][0] = u0[2 * nd[a]];
+    u0n[a][1] = u0[2 * nd[a] + 1];
+    B0n[a][0] = B0[2 * nd[a]];
+    B0n[a][1] = B0[2 * nd[a] + 1];
+  }
+  double gp[3][2];   // physical P1 gradients (constant)
+#pragma unroll
+  for (int v = 0; v < 3; ++v) {
+    gp[v][0] = tb.dpsi[2 * v] * J00 + tb.dpsi[2 * v + 1] * J10;
+    gp[v][1] = tb.dpsi[2 * v] * J01 + tb.dpsi[2 * v + 1] * J11;
+  }
+  double row[30];
+#pragma unroll
+  for (int j = 0; j < 30; ++j) row[j] = 0.0;
+  const double iRe = 1.0 / tb.Re, iRm = 1.0 / tb.Rm, Sc = tb.S;
+  for (int q = 0; q < tb.nq; ++q) {
+    const double wq = tb.w[q] * det;
+    double ph[6], G[6][2];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      ph[a] = tb.phi[q * 6 + a];
+      const double d0 = tb.dphi[(q * 6 + a) * 2], d1 = tb.dphi[(q * 6 + a) * 2 + 1];
+      G[a][0] = d0 * J00 + d1 * J10;
+      G[a][1] = d0 * J01 + d1 * J11;
+    }
+    double U[2] = {0.0, 0.0}, Bq[2] = {0.0, 0.0}, gU[2][2] = {{0.0, 0.0}, {0.0, 0.0}},
+           gB[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int a = 0; a < 6; ++a)
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        U[d] += u0n[a][d] * ph[a];
+        Bq[d] += B0n[a][d] * ph[a];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          gU[d][e] += u0n[a][d] * G[a][e];
+          gB[d][e] += B0n[a][d] * G[a][e];
+        }
+      }
+    const double j0 = gB[1][0] - gB[0][1];
+    const double zB0[2] = {-Bq[1], Bq[0]};     // z^ x B0
+    const double cB0[2] = {Bq[1], -Bq[0]};     // e_f x B0
+    const double cu0[2] = {-U[1], U[0]};       // u0 x e_g
+    if (i < 24) {
+      const int a = i >> 2, comp = i & 3;
+      const double jca[2] = {-G[a][1], G[a][0]};   // j(phi_a e_h)
+      for (int b = 0; b < 6; ++b) {
+        const double jcb[2] = {-G[b][1], G[b][0]};
+        const double lap = G[a][0] * G[b][0] + G[a][1] * G[b][1];
+        const double adv = ph[a] * (U[0] * G[b][0] + U[1] * G[b][1]);
+        if (comp < 2) {
+          const int d = comp;
+#pragma unroll
+          for (int f = 0; f < 2; ++f) {
+            // (1/Re)[delta_df grad.grad + d_f phi_a d_d phi_b] + convection
+            double v = iRe * ((d == f ? lap : 0.0) + G[a][f] * G[b][d]);
+            v += (d == f ? adv : 0.0) + ph[a] * ph[b] * gU[d][f];
+            row[4 * b + f] += wq * v;
+          }
+#pragma unroll
+          for (int g2 = 0; g2 < 2; ++g2) {
+            // -S [phi_a (z^xB0)_d j(phi_b e_g) + phi_a phi_b j0 (z^ x e_g)_d]
+            const double Zgd = (g2 == 0) ? (d == 1 ? 1.0 : 0.0) : (d == 0 ? -1.0 : 0.0);
+            row[4 * b + 2 + g2] += wq * (-Sc) * (ph[a] * zB0[d] * jcb[g2] + ph[a] * ph[b] * j0 * Zgd);
+          }
+        } else {
+          const int h = comp - 2;
+#pragma unroll
+          for (int f = 0; f < 2; ++f) row[4 * b + f] += wq * (-ph[b] * cB0[f] * jca[h]);
+#pragma unroll
+          for (int g2 = 0; g2 < 2; ++g2)
+            row[4 * b + 2 + g2] += wq * (-ph[b] * cu0[g2] * jca[h] + iRm * jcb[g2] * jca[h]);
+        }
+      }
+      if (comp < 2) {
+#pragma unroll
+        for (int v = 0; v < 3; ++v) row[27 + v] += wq * (-tb.psi[q * 3 + v] * G[a][comp]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < 3; ++v) row[24 + v] += wq * (-gp[v][comp - 2] * ph[a]);
+      }
+    } else if (i < 27) {
+      const int v = i - 24;   // -(B, grad s_v)
+      for (int b = 0; b < 6; ++b)
+#pragma unroll
+        for (int g2 = 0; g2 < 2; ++g2) row[4 * b + 2 + g2] += wq * (-ph[b] * gp[v][g2]);
+    } else {
+      const int v = i - 27;   // -(div u, q_v)
+      for (int b = 0; b < 6; ++b)
+#pragma unroll
+        for (int f = 0; f < 2; ++f) row[4 * b + f] += wq * (-tb.psi[q * 3 + v] * G[b][f]);
+    }
+  }
+  double* out = Le + (long)cell * 900 + i * 30;
+#pragma unroll
+  for (int j = 0; j < 30; ++j) out[j] = row[j];
+}
+
+__global__ void mhd_gather_kernel(int nnz, const int32_t* __restrict__ ptr,
+                                  const int32_t* __restrict__ contrib,
+                                  const double* __restrict__ Le, double* __restrict__ ml,
+                                  const int32_t* __restrict__ sell_pos, double* __restrict__ sml) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int k = ptr[e]; k < ptr[e + 1]; ++k) v += Le[contrib[k]];
+    ml[2L * e + 1] = v;
+    if (sml) sml[2L * sell_pos[e] + 1] = v;
+  }
+}
+
 }  // namespace ivk
 
 using namespace ivk;
@@ -228,6 +367,34 @@ int ivk_general_apply(const ivk_general_desc* op, const double* x, const double*
     case 3: general_apply_kernel<3><<<grid, kGenBlock, 0, st>>>(g, x, b, out); break;
   }
   return check_launch("ivk_general_apply");
+}
+
+int ivk_mhd_assemble(const ivk_mhd_desc* d, const double* u0, const double* B0,
+                     double* elem_scratch, double* ml, double* sml, void* stream) {
+  IVK_REQUIRE(d && u0 && B0 && elem_scratch && ml, "bad MHD assembly arguments");
+  IVK_REQUIRE(d->nq >= 1 && d->nq <= IVK_MHD_MAX_QUAD, "quadrature rule size");
+  IVK_REQUIRE(d->cell_geo && d->cell_nodes && d->entry_ptr && d->entry_contrib,
+              "MHD descriptor has a NULL array");
+  IVK_REQUIRE(!sml || d->sell_pos, "SELL output needs sell_pos");
+  MhdTables tb;
+  tb.nq = d->nq;
+  tb.Re = d->Re;
+  tb.Rm = d->Rm;
+  tb.S = d->S;
+  for (int i = 0; i < IVK_MHD_MAX_QUAD; ++i) tb.w[i] = d->w[i];
+  for (int i = 0; i < IVK_MHD_MAX_QUAD * 6; ++i) tb.phi[i] = d->phi[i];
+  for (int i = 0; i < IVK_MHD_MAX_QUAD * 12; ++i) tb.dphi[i] = d->dphi[i];
+  for (int i = 0; i < IVK_MHD_MAX_QUAD * 3; ++i) tb.psi[i] = d->psi[i];
+  for (int i = 0; i < 6; ++i) tb.dpsi[i] = d->dpsi[i];
+  cudaStream_t st = as_stream(stream);
+  const long nthr = (long)d->n_cells * 30;
+  mhd_element_kernel<<<(int)((nthr + 127) / 128), 128, 0, st>>>(tb, d->n_cells, d->cell_geo,
+                                                                 d->cell_nodes, u0, B0, elem_scratch);
+  int rc = check_launch("ivk_mhd_assemble(elements)");
+  if (rc) return rc;
+  mhd_gather_kernel<<<grid_cap(d->nnz, 256), 256, 0, st>>>(d->nnz, d->entry_ptr, d->entry_contrib,
+                                                           elem_scratch, ml, d->sell_pos, sml);
+  return check_launch("ivk_mhd_assemble(gather)");
 }
 
 int ivk_general_seed_constrained(const ivk_general_desc* op, const double* src, double* out,

@@ -160,6 +160,17 @@ class GeneralStageSystem:
     def desc(self):
         return self.device_data()["desc"]
 
+    def sell_pos(self):
+        """Position of every CSR entry in the SELL-32 copy (``to_sell``)."""
+        from .stages import sell_positions
+        return sell_positions(self.rowptr, self.n1, C=32)[1]
+
+    def download_operator(self):
+        """Refresh the host ``l`` from the device CSR after a device
+        re-linearisation (the coarse direct solve factorises on the host)."""
+        if self._dev is not None:
+            self.l = self._dev["tensors"]["ml"][:, 1].cpu().numpy().copy()
+
     def apply_into(self, x, b, out):
         """Device: out = b - A x (b is not None) or out = A x (K1g)."""
         from ._device import ptr, stream

@@ -35,14 +35,14 @@ P2 state x P1 gradient x P2 test).
 import numpy as np
 import scipy.sparse as sp
 
-from . import fem
+from . import _lib, fem
 from .fem import _affine, _coo_to_csr, _physical_gradients, p2_cell_nodes, p2_node_coords
 from .discretization import ConfigError, streamfunction_velocity
 from .mesh import build_hierarchy
 from .quadrature import p1_basis, p2_basis, triangle_rule
 
 __all__ = ["MHDParams", "MHDDiscretization", "assemble_mhd", "mhd_boundary_dofs",
-           "mhd_prolongation", "mhd_magnetic_state", "NCOMP_W"]
+           "mhd_prolongation", "mhd_magnetic_state", "MHDAssembler", "NCOMP_W"]
 
 NCOMP_W = 4          # (u_x, u_y, B_x, B_y) per scalar P2 node
 DEG_MHD = 5
@@ -175,12 +175,27 @@ def mhd_boundary_dofs(mesh, tol=1e-12):
     return np.unique(np.concatenate(out)).astype(np.int64)
 
 
+def element_structure():
+    """(30, 30) bool: the element couplings the linearised MHD form can make
+    nonzero for any state (u, B among themselves; u-p and B-r saddle pairs)."""
+    st = np.zeros((30, 30), dtype=bool)
+    st[:24, :24] = True
+    uu = np.arange(24)[np.arange(24) % 4 < 2]
+    bb = np.arange(24)[np.arange(24) % 4 >= 2]
+    st[np.ix_(uu, np.arange(27, 30))] = True
+    st[np.ix_(np.arange(27, 30), uu)] = True
+    st[np.ix_(bb, np.arange(24, 27))] = True
+    st[np.ix_(np.arange(24, 27), bb)] = True
+    return st
+
+
 def assemble_mhd(mesh, params, u0_func=streamfunction_velocity, B0_func=mhd_magnetic_state,
                  constrained=None):
     """Single-stage CSR (rowptr, col, m, l) of the mass and the linearised
     operator on one shared pattern, Dirichlet-eliminated (constrained rows
-    and columns zeroed; the stage operator puts identity rows there) and
-    with exact zeros dropped."""
+    and columns dropped; the stage operator puts identity rows there).  The
+    pattern is structural (``element_structure``), not value-dependent, so a
+    device re-linearisation (``MHDAssembler``) fills the same entries."""
     n_nodes, nv, n1 = _layout(mesh)
     xy = p2_node_coords(mesh)
     u0 = np.asarray(u0_func(xy), dtype=np.float64)
@@ -189,7 +204,7 @@ def assemble_mhd(mesh, params, u0_func=streamfunction_velocity, B0_func=mhd_magn
     dofs = cell_dofs(mesh)
     rows = np.repeat(dofs[:, :, None], 30, axis=2)
     cols = np.repeat(dofs[:, None, :], 30, axis=1)
-    nzr = (Me != 0.0) | (Le != 0.0)
+    nzr = np.broadcast_to(element_structure(), Me.shape)
     rowptr, col, ml = _coo_to_csr(rows[nzr], cols[nzr], np.stack([Me[nzr], Le[nzr]], axis=-1),
                                   n1, n1)
     if constrained is None:
@@ -197,11 +212,102 @@ def assemble_mhd(mesh, params, u0_func=streamfunction_velocity, B0_func=mhd_magn
     cmask = np.zeros(n1, dtype=bool)
     cmask[constrained] = True
     r_of = np.repeat(np.arange(n1), np.diff(rowptr))
-    keep = ~(cmask[r_of] | cmask[col]) & ((ml[:, 0] != 0.0) | (ml[:, 1] != 0.0))
+    keep = ~(cmask[r_of] | cmask[col])
     counts = np.bincount(r_of[keep], minlength=n1)
     rowptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
     return rowptr, col[keep], np.ascontiguousarray(ml[keep, 0]), \
         np.ascontiguousarray(ml[keep, 1]), cmask
+
+
+class MHDAssembler:
+    """Device re-linearisation of one level's operator L at a new frozen state
+    (K10g, ``ivk_mhd_assemble``): element rows by the formulas of
+    ``element_matrices``, then a deterministic per-entry gather (cell order,
+    the order ``assemble_mhd`` sums in) into the l half of the system's CSR
+    and SELL-32 (m, l) pairs.  The mass half and every index table of the
+    stage system, patches and transfers stay as they are."""
+
+    def __init__(self, mesh, params, system):
+        self.params = params
+        nodes = p2_cell_nodes(mesh)
+        _, jinv, det = _affine(mesh)
+        self.cell_nodes = nodes
+        self.cell_geo = np.column_stack([jinv.reshape(-1, 4), det])
+        C_ = len(nodes)
+        n1 = system.n1
+        cmask = system.cmask
+        dofs = cell_dofs(mesh)
+        ii, jj = np.nonzero(element_structure())
+        r, c = dofs[:, ii], dofs[:, jj]
+        contrib = np.arange(C_, dtype=np.int64)[:, None] * 900 + (ii * 30 + jj)[None, :]
+        keep = ~(cmask[r] | cmask[c])
+        key = (r.astype(np.int64) * n1 + c)[keep]
+        contrib = contrib[keep]
+        order = np.argsort(key, kind="stable")        # cell-ascending within an entry
+        rows = np.repeat(np.arange(n1), np.diff(system.rowptr))
+        pkey = rows.astype(np.int64) * n1 + system.col
+        if not np.array_equal(np.unique(key), pkey):
+            raise ValueError("cell connectivity does not match the operator pattern")
+        counts = np.bincount(np.searchsorted(pkey, key[order]), minlength=len(pkey))
+        self.entry_ptr = np.concatenate([[0], np.cumsum(counts)])
+        self.entry_contrib = contrib[order]
+        if self.entry_contrib.max(initial=0) >= 2 ** 31:
+            raise ValueError("level too large for 32-bit contribution indices")
+        self.sell_pos = system.sell_pos()
+        self.n_cells, self.nnz = C_, len(pkey)
+        self.n_nodes = system.n_nodes
+        pts, w = triangle_rule(DEG_MHD)
+        phi, dphi = p2_basis(pts)
+        psi, dpsi = p1_basis(pts)
+        d = _lib.MHDDesc()
+        d.n_cells, d.nnz, d.nq = C_, len(pkey), len(w)
+        if d.nq > _lib.IVK_MAX_QUAD:
+            raise ValueError("quadrature rule too large")
+        d.Re, d.Rm, d.S = params.Re, params.Rm, params.S
+        for q in range(d.nq):
+            d.w[q] = w[q]
+            for a in range(6):
+                d.phi[q * 6 + a] = phi[a, q]
+                d.dphi[(q * 6 + a) * 2] = dphi[a, q, 0]
+                d.dphi[(q * 6 + a) * 2 + 1] = dphi[a, q, 1]
+            for v in range(3):
+                d.psi[q * 3 + v] = psi[v, q]
+        for v in range(3):
+            d.dpsi[2 * v], d.dpsi[2 * v + 1] = dpsi[v, 0], dpsi[v, 1]
+        self.desc = d
+        self._dev = None
+
+    def _device(self):
+        if self._dev is None:
+            import torch
+            from ._device import upload
+            t = {"cell_geo": upload(self.cell_geo, np.float64),
+                 "cell_nodes": upload(self.cell_nodes, np.int32),
+                 "entry_ptr": upload(self.entry_ptr, np.int32),
+                 "entry_contrib": upload(self.entry_contrib, np.int32),
+                 "sell_pos": upload(self.sell_pos, np.int32)}
+            t["scratch"] = torch.empty(self.n_cells * 900, dtype=torch.float64,
+                                       device=t["cell_geo"].device)
+            d = self.desc
+            d.cell_geo, d.cell_nodes = t["cell_geo"].data_ptr(), t["cell_nodes"].data_ptr()
+            d.entry_ptr = t["entry_ptr"].data_ptr()
+            d.entry_contrib = t["entry_contrib"].data_ptr()
+            d.sell_pos = t["sell_pos"].data_ptr()
+            self._dev = t
+        return self._dev
+
+    def assemble_into_system(self, system, u0, B0):
+        """Overwrite ``system``'s device l values (CSR and SELL) with the
+        operator linearised about device nodal states u0, B0 ((n_nodes, 2) or
+        flat, this level's nodes)."""
+        from ._device import ptr, stream
+        t = self._device()
+        sd = system.device_data()["tensors"]
+        u0 = u0.reshape(-1)[:2 * self.n_nodes].contiguous()
+        B0 = B0.reshape(-1)[:2 * self.n_nodes].contiguous()
+        _lib.check(_lib.lib().ivk_mhd_assemble(self.desc, ptr(u0), ptr(B0), ptr(t["scratch"]),
+                                               ptr(sd["ml"]), ptr(sd["sml"]), stream()),
+                   "mhd_assemble")
 
 
 def mhd_prolongation(hier, level):
@@ -274,3 +380,28 @@ class MHDDiscretization:
             levels.append(MGLevel(system, patches, smoother, P))
         coarse = coarse_direct_solve(levels[0].system)
         return MGHierarchyOp(levels, coarse, use_graph=use_graph), levels[-1].system
+
+    def assembler(self, level, system):
+        key = ("asm", level)
+        if key not in self._stage_prolong:
+            self._stage_prolong[key] = MHDAssembler(self.hier.levels[level], self.params, system)
+        return self._stage_prolong[key]
+
+    def relinearize(self, mg, u0, B0):
+        """Re-linearise every level of ``mg`` about the fine-level device state
+        (u0, B0) -- (n_nodes, 2) nodal P2 values, injected to coarser levels as
+        the nodal prefix (nested P2 node numbering, as the reference's
+        ``inject_velocity``) -- then refactorise the smoothed levels' patches in
+        place (K7g) and rebuild the coarse direct solve: the Newton-cadence
+        update of config 5, all on the device but the coarse factorisation."""
+        from .solvers import coarse_direct_solve
+        start = self.num_levels - len(mg.levels)
+        for lv, lev in enumerate(mg.levels):
+            self.assembler(start + lv, lev.system).assemble_into_system(lev.system, u0, B0)
+            if lv > 0:
+                lev.patches.factor()
+        s0 = mg.levels[0].system
+        s0.download_operator()
+        mg.coarse = coarse_direct_solve(s0)
+        mg._graph = None
+        mg._bufs = None

@@ -18,6 +18,21 @@ from .fem import ConvectionBlocks, StokesBlocks
 __all__ = ["StageSystem", "assemble_stage_operator", "to_sell"]
 
 
+def sell_positions(rowptr, n_rows, C=32):
+    """(sptr, pos): the SELL-C slice pointers of ``to_sell`` and the position
+    of every CSR entry in the SELL arrays."""
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    lens = np.diff(rowptr)
+    nsl = (n_rows + C - 1) // C
+    padded = np.zeros(nsl * C, dtype=np.int64)
+    padded[:n_rows] = lens
+    width = padded.reshape(nsl, C).max(axis=1)
+    sptr = np.concatenate([[0], np.cumsum(width * C)])
+    rows = np.repeat(np.arange(n_rows), lens)
+    ent = np.arange(len(rows)) - rowptr[rows]
+    return sptr, sptr[rows // C] + ent * C + rows % C
+
+
 def to_sell(rowptr, col, vals, n_rows, pad_col=None, C=32):
     """CSR -> SELL-C (slices of C rows, entry e of a slice's lane-th row at
     ptr[slice] + C e + lane).  Padding entries get zero values and a valid

@@ -46,6 +46,7 @@ STRUCTS = {
     "ivk_quad_table": _lib.QuadTable,
     "ivk_convection_desc": _lib.ConvectionDesc,
     "ivk_general_desc": _lib.GeneralDesc,
+    "ivk_mhd_desc": _lib.MHDDesc,
     "ivk_general_transfer_desc": _lib.GeneralTransferDesc,
     "ivk_modal_desc": _lib.ModalDesc,
     "ivk_peer_view": _lib.PeerView,

@@ -149,3 +149,26 @@ def test_patch_vel_general_lists_p2_dofs():
         assert np.array_equal(idx[:len(single)], single)
         w = single[single < nw]
         assert len(single) - len(w) in (1, 2)        # p (and r unless on the boundary)
+
+
+def test_device_assembly_contribution_map():
+    """The (cell, row, column) -> CSR entry map the device re-linearisation
+    gathers through (MHDAssembler, K10g), summed on the host in its cell
+    order, reproduces assemble_mhd for a new state -- including the
+    structurally kept zeros."""
+    from paper_2202_07381_b200.mhd import MHDAssembler, element_matrices
+    disc, tab, case = mhd_setup("mhd16")
+    mesh = disc.fine_mesh
+    S = disc.system(disc.num_levels - 1, tab, case["dt"])
+    asm = MHDAssembler(mesh, disc.params, S)
+    n_nodes = S.n_nodes
+    rng = np.random.default_rng(11)
+    u1, B1 = rng.uniform(-1, 1, (n_nodes, 2)), rng.uniform(-1, 1, (n_nodes, 2))
+    _, Le = element_matrices(mesh, u1, B1, disc.params)
+    flat = Le.reshape(-1)[asm.entry_contrib]
+    ptr = asm.entry_ptr
+    got = np.array([flat[ptr[e]:ptr[e + 1]].sum() for e in range(len(ptr) - 1)])
+    rowptr, col, _, l, _ = assemble_mhd(mesh, disc.params, lambda xy: u1, lambda xy: B1)
+    assert np.array_equal(rowptr, S.rowptr) and np.array_equal(col, S.col)
+    assert np.max(np.abs(got - l)) <= 1e-14 * np.max(np.abs(l))
+    assert len(asm.sell_pos) == len(col)
