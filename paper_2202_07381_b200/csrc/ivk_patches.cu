@@ -13,6 +13,7 @@
 //                          memory (replaces np.linalg.inv, solvers.py:177).
 
 #include <climits>
+#include <cstdlib>
 
 #include "ivk_common.cuh"
 
@@ -988,10 +989,14 @@ struct ModalParams {
   double a[IVK_MAX_STAGES * IVK_MAX_STAGES];
 };
 
-// record: W_s rows with odd leading dimension k|1 (the shared-memory layout,
-// so one TMA bulk copy lands it ready to use), theta, c^, H^-1; 32-byte padded
+// record: W_s rows with leading dimension modal_ld(k) = 4 (mod 8) (the
+// shared-memory layout, so one TMA bulk copy lands it ready to use: the
+// tensor-core A fragments -- lane (g, q) reading row q, column g or the
+// transpose -- then hit 16 distinct 8-byte banks per half-warp), theta, c^,
+// H^-1; 32-byte padded
+__host__ __device__ __forceinline__ int modal_ld(int k) { return ((k + 3) >> 3) * 8 + 4; }
 __host__ __device__ __forceinline__ int modal_rec(int S, int NC, int k) {
-  return (k * (k | 1) + k + NC * k + S * S + 3) & ~3;
+  return (k * modal_ld(k) + k + NC * k + S * S + 3) & ~3;
 }
 template <int NC>
 __global__ void __launch_bounds__(128) patch_gather_blocks_kernel(FactorParams op, PatchParams pd,
@@ -1090,9 +1095,15 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
+// R and T rows use an odd stride TS = NA | 1 (the lane-per-mode phase reads
+// and writes row i in lane i: conflict-free banks); the tensor-core B loads
+// read the padded columns NA..NW-1 past the row end (finite values of the
+// next row or the NW slack, multiplied into output columns that are dropped).
+__host__ __device__ __forceinline__ int modal_tc_tbuf(int S, int NC, int KP) {
+  return KP * ((NC * S) | 1) + 8 * ((NC * S + 7) / 8);
+}
 __host__ __device__ __forceinline__ int modal_tc_seg(int S, int NC, int kmax, int KP) {
-  const int NW = 8 * ((NC * S + 7) / 8);
-  return (2 * modal_rec(S, NC, kmax) + 2 * KP * NW + 2 * 4 + KP * NW + KP * S * S + 3) & ~3;
+  return (2 * modal_rec(S, NC, kmax) + 2 * modal_tc_tbuf(S, NC, KP) + 2 * 4 + 3) & ~3;
 }
 
 template <int S, int NC, int KP>
@@ -1105,17 +1116,20 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
   constexpr int NT = (NA + 7) / 8;   // 8-column N tiles
   constexpr int NW = 8 * NT;         // padded row width of R / T
   constexpr int MT = KP / 8, KT = KP / 4;
+  constexpr int TS = NA | 1;                    // row stride of R and T
+  static_assert(KP <= 32, "one mode per lane");
+  constexpr int TBUF = KP * TS + NW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int gq = lane >> 2, gk = lane & 3;
   const int recmax = modal_rec(S, NC, kmax);
   double* buf0 = modal_sm + (long)warp * modal_tc_seg(S, NC, kmax, KP);
   double* buf1 = buf0 + recmax;
-  double* rsT0 = buf1 + recmax;      // R: [alpha][NW], zero padded rows / columns
-  double* rsT1 = rsT0 + KP * NW;
-  double* rsP = rsT1 + KP * NW;      // the s pressures, two buffers of 4
-  double* t = rsP + 8;               // T / w / v: [i][NW]
-  double* Es = t + KP * NW;
-  for (int e = lane; e < 3 * KP * NW; e += 32) rsT0[e] = 0.0;   // rsT0, rsT1, rsP, t
+  // R: [alpha][TS], zero rows past k.  One buffer: R is read only by the T
+  // GEMM, so the next patch's r values land in it after that.
+  double* rsT0 = buf1 + recmax;
+  double* rsP = rsT0 + TBUF;         // the s pressures, two buffers of 4
+  double* t = rsP + 8;               // T / w / v: [i][TS]
+  for (int e = lane; e < 2 * TBUF + 8; e += 32) rsT0[e] = 0.0;   // rsT0, rsP, t
   if (lane == 0) {
     mbar_init(&bars[warp][0], 1);
     mbar_init(&bars[warp][1], 1);
@@ -1144,7 +1158,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
       const double v = __ldg(r + pd.idx[off0 + j]);
       if (e < NC * k0) {
         const int al = e / NC, d = e - al * NC;
-        rsT0[al * NW + d * S + a] = v;
+        rsT0[al * TS + d * S + a] = v;
       } else {
         rsP[a] = v;
       }
@@ -1162,8 +1176,8 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
     const int off = pd.idx_off[p];
     const int k = pd.node_off[p + 1] - pd.node_off[p];
     const int blk = NC * k + 1;
-    const int ld = k | 1;
-    const double* R = slot ? rsT1 : rsT0;
+    const int ld = modal_ld(k);
+    const double* R = rsT0;
     const double* Rp = rsP + 4 * slot;
     // next patch: gather indices now, r values after step 1 (m <= 128 prefetched)
     int pf_idx[4];
@@ -1198,7 +1212,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
           const int al = 4 * kt + gk;
           double b[NT];
 #pragma unroll
-          for (int n = 0; n < NT; ++n) b[n] = R[al * NW + 8 * n + gq];
+          for (int n = 0; n < NT; ++n) b[n] = R[al * TS + 8 * n + gq];
 #pragma unroll
           for (int m = 0; m < MT; ++m) {
             const int i = 8 * m + gq;
@@ -1212,35 +1226,38 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
       for (int m = 0; m < MT; ++m)
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
-          double2 v2 = make_double2(d[m][n][0], d[m][n][1]);
-          *reinterpret_cast<double2*>(t + (8 * m + gq) * NW + 8 * n + 2 * gk) = v2;
+          const int q0 = 8 * n + 2 * gk;
+          if (q0 < NA) t[(8 * m + gq) * TS + q0] = d[m][n][0];
+          if (q0 + 1 < NA) t[(8 * m + gq) * TS + q0 + 1] = d[m][n][1];
         }
     }
     __syncwarp();
     double pf_val[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) pf_val[u] = pf_idx[u] >= 0 ? __ldg(r + pf_idx[u]) : 0.0;
-    // lane per mode i: w_i = E_i t_i, g += c^ w
+    // lane per mode i (k <= KP <= 32: one mode per lane): w_i = E_i t_i,
+    // g += c^ w; E_i, w_i and c^_i stay in registers across the reduction
+    const int im = lane;
+    const bool act = im < k;
+    double E[S * S], wv[NA], cc[NC];
     double g[S];
 #pragma unroll
     for (int a = 0; a < S; ++a) g[a] = 0.0;
-    for (int i = lane; i < k; i += 32) {
+    if (act) {
       double acc[NA];
-      lds_vec<NA>(t + i * NW, acc);
-      double E[S * S];
-      modal_small_inv<S>(mp.a, dt * th[i], E);
 #pragma unroll
-      for (int e = 0; e < S * S; ++e) Es[i * S * S + e] = E[e];
+      for (int q = 0; q < NA; ++q) acc[q] = t[im * TS + q];
+      modal_small_inv<S>(mp.a, dt * th[im], E);
 #pragma unroll
       for (int dd = 0; dd < NC; ++dd) {
-        const double c = ch[i * NC + dd];
+        cc[dd] = ch[im * NC + dd];
 #pragma unroll
         for (int a = 0; a < S; ++a) {
           double w = 0.0;
 #pragma unroll
           for (int b = 0; b < S; ++b) w = fma(E[a * S + b], acc[dd * S + b], w);
-          t[i * NW + dd * S + a] = w;
-          g[a] = fma(c, w, g[a]);
+          wv[dd * S + a] = w;
+          g[a] = fma(cc[dd], w, g[a]);
         }
       }
     }
@@ -1272,21 +1289,19 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
       for (int b = 0; b < S; ++b) s_ = fma(mp.a[a * S + b], pv[b], s_);
       Ap[a] = s_;
     }
-    for (int i = lane; i < k; i += 32) {
+    if (act) {
       double e[S];
 #pragma unroll
       for (int a = 0; a < S; ++a) {
         double s_ = 0.0;
 #pragma unroll
-        for (int b = 0; b < S; ++b) s_ = fma(Es[i * S * S + a * S + b], Ap[b], s_);
+        for (int b = 0; b < S; ++b) s_ = fma(E[a * S + b], Ap[b], s_);
         e[a] = s_;
       }
 #pragma unroll
-      for (int dd = 0; dd < NC; ++dd) {
-        const double c = dt * ch[i * NC + dd];
+      for (int dd = 0; dd < NC; ++dd)
 #pragma unroll
-        for (int a = 0; a < S; ++a) t[i * NW + dd * S + a] = fma(-c, e[a], t[i * NW + dd * S + a]);
-      }
+        for (int a = 0; a < S; ++a) t[im * TS + dd * S + a] = fma(-dt * cc[dd], e[a], wv[dd * S + a]);
     }
     __syncwarp();
     // U = W V; each lane writes its two D entries of every tile
@@ -1302,7 +1317,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
           const int i = 4 * kt + gk;
           double b[NT];
 #pragma unroll
-          for (int n = 0; n < NT; ++n) b[n] = t[i * NW + 8 * n + gq];
+          for (int n = 0; n < NT; ++n) b[n] = t[i * TS + 8 * n + gq];
 #pragma unroll
           for (int m = 0; m < MT; ++m) {
             const int al = 8 * m + gq;
@@ -1342,9 +1357,9 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
     // land the next patch's r values; clear the rows a previous (larger)
     // patch left behind, so the tensor-core tiles read zeros past k
     {
-      double* RN = slot ? rsT0 : rsT1;
+      double* RN = rsT0;
       double* RPN = rsP + 4 * (slot ^ 1);
-      for (int e = pn_k * NW + lane; e < KP * NW; e += 32) RN[e] = 0.0;
+      for (int e = pn_k * TS + lane; e < KP * TS; e += 32) RN[e] = 0.0;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int j = lane + 32 * u;
@@ -1353,7 +1368,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
           const int e = j - a * pn_blk;
           if (e < NC * pn_k) {
             const int al = e / NC, dd = e - al * NC;
-            RN[al * NW + dd * S + a] = pf_val[u];
+            RN[al * TS + dd * S + a] = pf_val[u];
           } else {
             RPN[a] = pf_val[u];
           }
@@ -1365,7 +1380,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
         const double v = __ldg(r + pd.idx[pn_off + j]);
         if (e < NC * pn_k) {
           const int al = e / NC, dd = e - al * NC;
-          RN[al * NW + dd * S + a] = v;
+          RN[al * TS + dd * S + a] = v;
         } else {
           RPN[a] = v;
         }
@@ -1454,7 +1469,7 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
     const int off = pd.idx_off[p];
     const int k = pd.node_off[p + 1] - pd.node_off[p];
     const int blk = NC * k + 1;
-    const int ld = k | 1;
+    const int ld = modal_ld(k);
     const double* R = slot ? R1 : R0;
     const double* Rpc = Rp + 4 * slot;
     int pf_idx[PF];
@@ -2490,8 +2505,22 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       return IVK_EUNSUPPORTED;
     }
     seg = seg_tc;
-    // warps per CTA: three CTAs per SM when the per-warp buffers allow it
-    int nw = (int)((72 * 1024) / seg);
+    // CTA shape: cps CTAs per SM, each as many warps as both the per-warp
+    // buffers (cta_kb of shared memory) and the register file allow -- the
+    // kernel is bound by its shared-memory pipe, not by latency, so more
+    // resident warps past ~15 per SM do not help (measured: 16 warps in two
+    // CTAs are 6% slower than 15 in three).  Env overrides for A/B runs.
+    static const int cta_kb = getenv("IVK_MODAL_CTA_KB") ? atoi(getenv("IVK_MODAL_CTA_KB")) : 72;
+    static const int cps = getenv("IVK_MODAL_CPS") ? atoi(getenv("IVK_MODAL_CPS")) : 3;
+    int nw = (int)((cta_kb * 1024) / seg);
+    {
+      cudaFuncAttributes fa;
+      if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess && fa.numRegs > 0) {
+        const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;   // 256-register granules
+        const int reg_nw = 65536 / regs_warp / cps;
+        if (nw > reg_nw) nw = reg_nw;
+      }
+    }
     if (nw > kApplyWarps) nw = kApplyWarps;
     if (nw < 1) nw = 1;
     IVK_REQUIRE(seg <= 200 * 1024, "modal patch (k = %d) exceeds shared memory", kmax);
@@ -2504,7 +2533,7 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       }
     }
     int mgrid = (pd->num_patches + nw - 1) / nw;
-    const int cap = kSMs * 3;
+    const int cap = kSMs * cps;
     if (mgrid > cap) mgrid = cap;
     fn<<<mgrid, nw * 32, smem, st>>>(p, mp, r, local, kmax);
     return check_launch("ivk_patch_apply(modal)");

@@ -20,7 +20,14 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["ModalSplit"]
+__all__ = ["ModalSplit", "modal_ld"]
+
+
+def modal_ld(k):
+    """Leading dimension of W_s in a record: k rounded up to 4 (mod 8), so the
+    K3m tensor-core A-fragment loads are bank-conflict free (ivk_patches.cu
+    modal_ld)."""
+    return ((k + 3) // 8) * 8 + 4
 
 
 def _bitwise_classes(rows):
@@ -53,13 +60,13 @@ class ModalSplit:
         self.nc = int(ncomp)
 
     def record_doubles(self, k):
-        return (k * (k | 1) + k + self.nc * k + self.s * self.s + 3) & ~3
+        return (k * modal_ld(k) + k + self.nc * k + self.s * self.s + 3) & ~3
 
     def _pack(self, W, theta, chat, Hinv, lib):
-        """Records (count, record_doubles(k)): W_s rows padded to the odd
-        leading dimension k|1 (the kernel's shared-memory layout)."""
+        """Records (count, record_doubles(k)): W_s rows padded to the
+        leading dimension ``modal_ld(k)`` (the kernel's shared-memory layout)."""
         count, k = W.shape[0], W.shape[1]
-        ld = k | 1
+        ld = modal_ld(k)
         if ld != k:
             W = lib.cat([W, W.new_zeros((count, k, ld - k))], dim=2) if hasattr(lib, "cat") \
                 else np.concatenate([W, np.zeros((count, k, ld - k))], axis=2)
@@ -160,7 +167,7 @@ class ModalSplit:
         return self._pack(W[None], theta[None], chat[None], np.linalg.inv(H)[None], np)[0]
 
     def unpack(self, raw, k):
-        nc, s, ld = self.nc, self.s, k | 1
+        nc, s, ld = self.nc, self.s, modal_ld(k)
         o = k * ld
         W = raw[:o].reshape(k, ld)[:, :k]
         th = raw[o:o + k]
