@@ -1129,7 +1129,11 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
   double* rsT0 = buf1 + recmax;
   double* rsP = rsT0 + TBUF;         // the s pressures, two buffers of 4
   double* t = rsP + 8;               // T / w / v: [i][TS]
-  for (int e = lane; e < 2 * TBUF + 8; e += 32) rsT0[e] = 0.0;   // rsT0, rsP, t
+  // zero the whole segment once: the tensor-core A loads below are not
+  // predicated, so they read (finite) record tails, the other buffer and
+  // stale rows past k -- every such value meets an exact zero in B
+  for (int e = lane; e < modal_tc_seg(S, NC, kmax, KP); e += 32) buf0[e] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // before TMA overwrites
   if (lane == 0) {
     mbar_init(&bars[warp][0], 1);
     mbar_init(&bars[warp][1], 1);
@@ -1215,8 +1219,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
           for (int n = 0; n < NT; ++n) b[n] = R[al * TS + 8 * n + gq];
 #pragma unroll
           for (int m = 0; m < MT; ++m) {
-            const int i = 8 * m + gq;
-            const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+            const double a = W[al * ld + 8 * m + gq];   // rows al >= k meet R's zero rows
 #pragma unroll
             for (int n = 0; n < NT; ++n) dmma884(d[m][n][0], d[m][n][1], a, b[n]);
           }
@@ -1302,6 +1305,10 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
       for (int dd = 0; dd < NC; ++dd)
 #pragma unroll
         for (int a = 0; a < S; ++a) t[im * TS + dd * S + a] = fma(-dt * cc[dd], e[a], wv[dd * S + a]);
+    } else if (im < KP) {
+      // rows past k: exact zeros for the U GEMM's unpredicated A columns
+#pragma unroll
+      for (int q = 0; q < NA; ++q) t[im * TS + q] = 0.0;
     }
     __syncwarp();
     // U = W V; each lane writes its two D entries of every tile
@@ -1320,8 +1327,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
           for (int n = 0; n < NT; ++n) b[n] = t[i * TS + 8 * n + gq];
 #pragma unroll
           for (int m = 0; m < MT; ++m) {
-            const int al = 8 * m + gq;
-            const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+            const double a = W[(8 * m + gq) * ld + i];   // columns i >= k meet t's zero rows
 #pragma unroll
             for (int n = 0; n < NT; ++n) dmma884(d[m][n][0], d[m][n][1], a, b[n]);
           }
