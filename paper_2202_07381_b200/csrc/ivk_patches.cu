@@ -1404,8 +1404,9 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
 constexpr int kModalCtaWarps = 16;
 
 __host__ __device__ __forceinline__ int modal_cta_smem(int S, int NC, int kmax, int KP) {
-  return (2 * modal_rec(S, NC, kmax) + 3 * modal_tc_tbuf(S, NC, KP) + 8 + kModalCtaWarps * 4 + 8 +
-          3) & ~3;
+  const int NW = 8 * ((NC * S + 7) / 8);
+  return (2 * modal_rec(S, NC, kmax) + 2 * KP * NW + 8 + KP * NW + KP * S * S +
+          kModalCtaWarps * 4 + 8 + 3) & ~3;
 }
 
 template <int S, int NC, int KP>
@@ -1419,9 +1420,6 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
   constexpr int NW = 8 * NT;
   constexpr int MT = KP / 8, KT = KP / 4;
   constexpr int NTH = kModalCtaWarps * 32;
-  constexpr int TS = NA | 1;        // odd row stride of R / T (thread-per-mode phase)
-  constexpr int TBUF = KP * TS + NW;
-  static_assert(KP <= NTH, "one mode per thread");
   constexpr int PF = 4;             // prefetched r values per thread (m <= 512)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, gk = lane & 3;
@@ -1429,12 +1427,13 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
   double* buf0 = modal_sm;
   double* buf1 = buf0 + recmax;
   double* R0 = buf1 + recmax;
-  double* R1 = R0 + TBUF;
-  double* Rp = R1 + TBUF;           // 2 x 4 pressures
+  double* R1 = R0 + KP * NW;
+  double* Rp = R1 + KP * NW;        // 2 x 4 pressures
   double* t = Rp + 8;
-  double* gred = t + TBUF;          // kModalCtaWarps x 4 partial sums
+  double* Es = t + KP * NW;
+  double* gred = Es + KP * S * S;   // kModalCtaWarps x 4 partial sums
   double* pAp = gred + kModalCtaWarps * 4;  // p (4) and A p (4)
-  for (int e = tid; e < 3 * TBUF + 8; e += NTH) R0[e] = 0.0;
+  for (int e = tid; e < 2 * KP * NW + 8 + KP * NW; e += NTH) R0[e] = 0.0;
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -1457,7 +1456,7 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
       const double v = __ldg(r + pd.idx[off0 + j]);
       if (e < NC * k0) {
         const int al = e / NC, d = e - al * NC;
-        R0[al * TS + d * S + a] = v;
+        R0[al * NW + d * S + a] = v;
       } else {
         Rp[a] = v;
       }
@@ -1510,14 +1509,11 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
         const int al = 4 * kt + gk;
         const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
 #pragma unroll
-        for (int n = 0; n < NT; ++n) dmma884(d[n][0], d[n][1], a, R[al * TS + 8 * n + gq]);
+        for (int n = 0; n < NT; ++n) dmma884(d[n][0], d[n][1], a, R[al * NW + 8 * n + gq]);
       }
 #pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        const int q0 = 8 * n + 2 * gk;
-        if (q0 < NA) t[i * TS + q0] = d[n][0];
-        if (q0 + 1 < NA) t[i * TS + q0 + 1] = d[n][1];
-      }
+      for (int n = 0; n < NT; ++n)
+        *reinterpret_cast<double2*>(t + i * NW + 8 * n + 2 * gk) = make_double2(d[n][0], d[n][1]);
     }
     double pf_val[PF];
 #pragma unroll
@@ -1527,25 +1523,23 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
     double g[S];
 #pragma unroll
     for (int a = 0; a < S; ++a) g[a] = 0.0;
-    // (k <= KP <= NTH: one mode per thread; E_i, w_i, c^_i stay in registers)
-    const bool act = tid < k;
-    double E[S * S], wv[NA], cc[NC];
-    if (act) {
-      const int i = tid;
+    for (int i = tid; i < k; i += NTH) {
       double acc[NA];
-#pragma unroll
-      for (int q = 0; q < NA; ++q) acc[q] = t[i * TS + q];
+      lds_vec<NA>(t + i * NW, acc);
+      double E[S * S];
       modal_small_inv<S>(mp.a, dt * th[i], E);
 #pragma unroll
+      for (int e = 0; e < S * S; ++e) Es[i * S * S + e] = E[e];
+#pragma unroll
       for (int dd = 0; dd < NC; ++dd) {
-        cc[dd] = ch[i * NC + dd];
+        const double c = ch[i * NC + dd];
 #pragma unroll
         for (int a = 0; a < S; ++a) {
           double w = 0.0;
 #pragma unroll
           for (int b = 0; b < S; ++b) w = fma(E[a * S + b], acc[dd * S + b], w);
-          wv[dd * S + a] = w;
-          g[a] = fma(cc[dd], w, g[a]);
+          t[i * NW + dd * S + a] = w;
+          g[a] = fma(c, w, g[a]);
         }
       }
     }
@@ -1590,20 +1584,21 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
       }
     }
     __syncthreads();
-    if (act) {
-      const int i = tid;
+    for (int i = tid; i < k; i += NTH) {
       double e[S];
 #pragma unroll
       for (int a = 0; a < S; ++a) {
         double s_ = 0.0;
 #pragma unroll
-        for (int b = 0; b < S; ++b) s_ = fma(E[a * S + b], pAp[4 + b], s_);
+        for (int b = 0; b < S; ++b) s_ = fma(Es[i * S * S + a * S + b], pAp[4 + b], s_);
         e[a] = s_;
       }
 #pragma unroll
-      for (int dd = 0; dd < NC; ++dd)
+      for (int dd = 0; dd < NC; ++dd) {
+        const double c = dt * ch[i * NC + dd];
 #pragma unroll
-        for (int a = 0; a < S; ++a) t[i * TS + dd * S + a] = fma(-dt * cc[dd], e[a], wv[dd * S + a]);
+        for (int a = 0; a < S; ++a) t[i * NW + dd * S + a] = fma(-c, e[a], t[i * NW + dd * S + a]);
+      }
     }
     __syncthreads();
     // U = W V: warp w takes node tiles w, w + 4, ...
@@ -1619,7 +1614,7 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
         const int i = 4 * kt + gk;
         const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
 #pragma unroll
-        for (int n = 0; n < NT; ++n) dmma884(d[n][0], d[n][1], a, t[i * TS + 8 * n + gq]);
+        for (int n = 0; n < NT; ++n) dmma884(d[n][0], d[n][1], a, t[i * NW + 8 * n + gq]);
       }
       if (al < k) {
 #pragma unroll
@@ -1644,7 +1639,7 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
     {
       double* RN = slot ? R0 : R1;
       double* RPN = Rp + 4 * (slot ^ 1);
-      for (int e = pn_k * TS + tid; e < KP * TS; e += NTH) RN[e] = 0.0;
+      for (int e = pn_k * NW + tid; e < KP * NW; e += NTH) RN[e] = 0.0;
 #pragma unroll
       for (int u = 0; u < PF; ++u) {
         const int j = tid + NTH * u;
@@ -1653,7 +1648,7 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
           const int e = j - a * pn_blk;
           if (e < NC * pn_k) {
             const int al = e / NC, dd = e - al * NC;
-            RN[al * TS + dd * S + a] = pf_val[u];
+            RN[al * NW + dd * S + a] = pf_val[u];
           } else {
             RPN[a] = pf_val[u];
           }
@@ -1665,7 +1660,7 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
         const double v = __ldg(r + pd.idx[pn_off + j]);
         if (e < NC * pn_k) {
           const int al = e / NC, dd = e - al * NC;
-          RN[al * TS + dd * S + a] = v;
+          RN[al * NW + dd * S + a] = v;
         } else {
           RPN[a] = v;
         }
