@@ -465,6 +465,27 @@ def run_ours(args, rank, world, local):
         for h in (mg, mg_pou):
             h._graph = None
 
+    # MHD (cfg5): Newton-cadence re-linearisation of the frozen state on the
+    # device (K10g per level + K7g refactor + coarse rebuild), at the same state
+    if relin is None and getattr(disc, "relinearize", None) is not None and \
+            hasattr(disc, "assembler"):
+        from paper_2202_07381_b200.discretization import streamfunction_velocity
+        from paper_2202_07381_b200.fem import p2_node_coords
+        from paper_2202_07381_b200.mhd import mhd_magnetic_state
+        xy = p2_node_coords(disc.fine_mesh)
+        u0 = torch.from_numpy(streamfunction_velocity(xy)).cuda()
+        B0 = torch.from_numpy(mhd_magnetic_state(xy)).cuda()
+        disc.relinearize(mg, u0, B0)     # first call uploads the assembly maps
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        disc.relinearize(mg, u0, B0)
+        torch.cuda.synchronize()
+        relin = {"seconds": time.perf_counter() - t0,
+                 "what": "MHD L(u0, B0) on all levels (K10g) + K7g refactor + coarse rebuild"}
+        mg_pou.coarse = mg.coarse
+        for h in (mg, mg_pou):
+            h._graph = None
+
     # One full IRK Newton step of Navier-Stokes on the device (newton.py,
     # SURVEY.md §8(f) #3): per-stage J_N on every level (K10), K7 refactor,
     # FGMRES + V-cycle per Newton iteration, u_n = the config's advecting field
