@@ -333,6 +333,7 @@ class MHDDiscretization:
                                  layout=_layout(m)))
         self._prolong = [mhd_prolongation(self.hier, k) for k in range(self.hier.num_levels - 1)]
         self._stage_prolong = {}
+        self._assemblers = {}
 
     @property
     def num_levels(self):
@@ -382,10 +383,11 @@ class MHDDiscretization:
         return MGHierarchyOp(levels, coarse, use_graph=use_graph), levels[-1].system
 
     def assembler(self, level, system):
-        key = ("asm", level)
-        if key not in self._stage_prolong:
-            self._stage_prolong[key] = MHDAssembler(self.hier.levels[level], self.params, system)
-        return self._stage_prolong[key]
+        """The level's device assembler (its maps depend only on the level's
+        operator pattern, shared by every stage system built on it)."""
+        if level not in self._assemblers:
+            self._assemblers[level] = MHDAssembler(self.hier.levels[level], self.params, system)
+        return self._assemblers[level]
 
     def relinearize(self, mg, u0, B0):
         """Re-linearise every level of ``mg`` about the fine-level device state
