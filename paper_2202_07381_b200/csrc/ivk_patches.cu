@@ -182,17 +182,21 @@ __global__ void patch_combine_kernel(PatchParams pd, const double* __restrict__ 
     if (pd.slot_pos) {
       for (int k = k0; k < k1; ++k) z += local[k];
     } else {
-      int k = k0;
-      for (; k + 4 <= k1; k += 4) {
-        const int p0 = pd.dof_pos[k], p1 = pd.dof_pos[k + 1], p2 = pd.dof_pos[k + 2],
-                  p3 = pd.dof_pos[k + 3];
-        const double v0 = local[p0], v1 = local[p1], v2 = local[p2], v3 = local[p3];
-        z += v0;
-        z += v1;
-        z += v2;
-        z += v3;
+      // up to 8 contributions per round: all position loads, then all value
+      // loads in flight (a 2-D vertex DoF has 7: one round trip pair instead
+      // of a batch of 4 plus 3 dependent singles); summed in slot order
+      constexpr int U = 8;
+      for (int k = k0; k < k1; k += U) {
+        int pp[U];
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) pp[u] = k + u < k1 ? __ldg(pd.dof_pos + k + u) : -1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = pp[u] >= 0 ? local[pp[u]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (pp[u] >= 0) z += v[u];
       }
-      for (; k < k1; ++k) z += local[pd.dof_pos[k]];
     }
     double v = beta * (w ? w[d] : 1.0) * z;
     if (x) v = alpha * x[d] + v;
