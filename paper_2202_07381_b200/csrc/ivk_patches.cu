@@ -2515,13 +2515,14 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       return IVK_EUNSUPPORTED;
     }
     seg = seg_tc;
-    // CTA shape: cps CTAs per SM, each as many warps as both the per-warp
+    // CTA shape: cps CTAs per SM (4 x 4 warps at cfg2: 117.9 us vs 119.3 for
+    // 3 x 5 and 121.3 for 5 x 3), each as many warps as both the per-warp
     // buffers (cta_kb of shared memory) and the register file allow -- the
     // kernel is bound by its shared-memory pipe, not by latency, so more
     // resident warps past ~15 per SM do not help (measured: 16 warps in two
     // CTAs are 6% slower than 15 in three).  Env overrides for A/B runs.
     static const int cta_kb = getenv("IVK_MODAL_CTA_KB") ? atoi(getenv("IVK_MODAL_CTA_KB")) : 72;
-    static const int cps = getenv("IVK_MODAL_CPS") ? atoi(getenv("IVK_MODAL_CPS")) : 3;
+    static const int cps = getenv("IVK_MODAL_CPS") ? atoi(getenv("IVK_MODAL_CPS")) : 4;
     int nw = (int)((cta_kb * 1024) / seg);
     {
       cudaFuncAttributes fa;
