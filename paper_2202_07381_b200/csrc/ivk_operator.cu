@@ -61,8 +61,12 @@ struct OpParams {
 // NC = 0 (Stokes), 1 (one J shared by all stages) or S (per-stage J_i).
 // LIST: only the warps (slices) listed in `slices` run -- the rows a shard's
 // patches read (shard.py); the other rows of `out` are left untouched.
+// The Stokes full-grid variant (S >= 2) is capped at 64 registers (4 CTAs, 32 warps
+// per SM): its software-pipelined gathers need 78 otherwise, and the lost
+// occupancy costs more than the pipelining gains (57 -> 60 us uncapped, 51.6
+// capped, cfg2 fine level).
 template <int S, int NC, bool LIST>
-__global__ void __launch_bounds__(256) stage_apply_kernel(OpParams op, const double* __restrict__ x,
+__global__ void __launch_bounds__(256, (NC == 0 && !LIST && S >= 2) ? 4 : 0) stage_apply_kernel(OpParams op, const double* __restrict__ x,
                                                           const double* __restrict__ b,
                                                           double* __restrict__ out,
                                                           const int32_t* __restrict__ slices,
@@ -98,6 +102,47 @@ __global__ void __launch_bounds__(256) stage_apply_kernel(OpParams op, const dou
         // latency-bound gathers: U entries' (col, m/k) loads, then their 3 U
         // x loads, in flight together (same summation order as one by one)
         constexpr int U = 4;
+        if constexpr (!LIST && S >= 2) {
+        // software pipeline: the next batch's (col, m/k) loads are issued
+        // before this batch's x gathers are consumed
+        int cl[U];
+        double2 mk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int ee = e0 + j + 16 * u;
+          const bool ok = ee < e1;
+          cl[u] = ok ? op.p2_scol[ee] : -1;
+          mk[u] = ok ? op.p2_smk[ee] : make_double2(0.0, 0.0);
+        }
+        for (int e = e0 + j; e < e1; e += 16 * U) {
+          double uu[U][S];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int t = 0; t < S; ++t) uu[u][t] = cl[u] >= 0 ? x[t * sd + 2 * cl[u] + c] : 0.0;
+          int cn[U];
+          double2 mn[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int ee = e + 16 * (U + u);
+            const bool ok = ee < e1;
+            cn[u] = ok ? op.p2_scol[ee] : -1;
+            mn[u] = ok ? op.p2_smk[ee] : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int t = 0; t < S; ++t) {
+              mu[t] = fma(mk[u].x, uu[u][t], mu[t]);
+              ku[t] = fma(mk[u].y, uu[u][t], ku[t]);
+            }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            cl[u] = cn[u];
+            mk[u] = mn[u];
+          }
+        }
+        } else {
         for (int e = e0 + j; e < e1; e += 16 * U) {
           int cl[U];
           double2 mk[U];
@@ -120,6 +165,7 @@ __global__ void __launch_bounds__(256) stage_apply_kernel(OpParams op, const dou
               mu[t] = fma(mk[u].x, uu[u][t], mu[t]);
               ku[t] = fma(mk[u].y, uu[u][t], ku[t]);
             }
+        }
         }
       } else
 #pragma unroll 2
@@ -211,6 +257,47 @@ __global__ void __launch_bounds__(256) stage_apply_kernel(OpParams op, const dou
     for (int t = 0; t < S; ++t) btu[t] = 0.0;
     const int e0 = op.bt_sptr[ws], e1 = op.bt_sptr[ws + 1];
     constexpr int U = 4;
+#ifdef IVK_K1_PIPE_BT
+    int nn[U];
+    double2 bv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int ee = e0 + lane + 32 * u;
+      const bool ok = ee < e1;
+      nn[u] = ok ? op.bt_scol[ee] : -1;
+      bv[u] = ok ? op.bt_sval[ee] : make_double2(0.0, 0.0);
+    }
+    for (int e = e0 + lane; e < e1; e += 32 * U) {
+      double2 xv[U][S];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int t = 0; t < S; ++t)
+          xv[u][t] = nn[u] >= 0 ? make_double2(x[t * sd + 2 * nn[u]], x[t * sd + 2 * nn[u] + 1])
+                                : make_double2(0.0, 0.0);
+      int nx[U];
+      double2 bx[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int ee = e + 32 * (U + u);
+        const bool ok = ee < e1;
+        nx[u] = ok ? op.bt_scol[ee] : -1;
+        bx[u] = ok ? op.bt_sval[ee] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          btu[t] = fma(bv[u].x, xv[u][t].x, btu[t]);
+          btu[t] = fma(bv[u].y, xv[u][t].y, btu[t]);
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        nn[u] = nx[u];
+        bv[u] = bx[u];
+      }
+    }
+#else
     for (int e = e0 + lane; e < e1; e += 32 * U) {
       int nn[U];
       double2 bv[U];
@@ -237,6 +324,7 @@ __global__ void __launch_bounds__(256) stage_apply_kernel(OpParams op, const dou
           btu[t] = fma(bv[u].y, xv[u][t].y, btu[t]);
         }
     }
+#endif
     if (q >= op.n_p) return;
 #pragma unroll
     for (int i = 0; i < S; ++i) {

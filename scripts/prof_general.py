@@ -49,7 +49,7 @@ def main(name, n, mode="kron"):
     t /= max(n - 2, 1)
     print(f"{name}: mode {pat.mode}, K1 {1e3 * t[0]:.1f} us, K3 {1e3 * t[1]:.1f} us, "
           f"K4 {1e3 * t[2]:.1f} us, inverse store {8 * pat.inv_size / 1e9:.3f} GB, "
-          f"finite {bool(torch.isfinite(x).all())}")
+          f"finite {bool(torch.isfinite(x).all())}, r checksum {float(r.abs().sum())!r}")
 
 
 if __name__ == "__main__":
