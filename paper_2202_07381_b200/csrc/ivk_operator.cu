@@ -257,47 +257,6 @@ __global__ void __launch_bounds__(256, (NC == 0 && !LIST && S >= 2) ? 4 : 0) sta
     for (int t = 0; t < S; ++t) btu[t] = 0.0;
     const int e0 = op.bt_sptr[ws], e1 = op.bt_sptr[ws + 1];
     constexpr int U = 4;
-#ifdef IVK_K1_PIPE_BT
-    int nn[U];
-    double2 bv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int ee = e0 + lane + 32 * u;
-      const bool ok = ee < e1;
-      nn[u] = ok ? op.bt_scol[ee] : -1;
-      bv[u] = ok ? op.bt_sval[ee] : make_double2(0.0, 0.0);
-    }
-    for (int e = e0 + lane; e < e1; e += 32 * U) {
-      double2 xv[U][S];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int t = 0; t < S; ++t)
-          xv[u][t] = nn[u] >= 0 ? make_double2(x[t * sd + 2 * nn[u]], x[t * sd + 2 * nn[u] + 1])
-                                : make_double2(0.0, 0.0);
-      int nx[U];
-      double2 bx[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int ee = e + 32 * (U + u);
-        const bool ok = ee < e1;
-        nx[u] = ok ? op.bt_scol[ee] : -1;
-        bx[u] = ok ? op.bt_sval[ee] : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int t = 0; t < S; ++t) {
-          btu[t] = fma(bv[u].x, xv[u][t].x, btu[t]);
-          btu[t] = fma(bv[u].y, xv[u][t].y, btu[t]);
-        }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        nn[u] = nx[u];
-        bv[u] = bx[u];
-      }
-    }
-#else
     for (int e = e0 + lane; e < e1; e += 32 * U) {
       int nn[U];
       double2 bv[U];
@@ -324,7 +283,6 @@ __global__ void __launch_bounds__(256, (NC == 0 && !LIST && S >= 2) ? 4 : 0) sta
           btu[t] = fma(bv[u].y, xv[u][t].y, btu[t]);
         }
     }
-#endif
     if (q >= op.n_p) return;
 #pragma unroll
     for (int i = 0; i < S; ++i) {
