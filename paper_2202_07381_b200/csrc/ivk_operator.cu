@@ -101,7 +101,12 @@ __global__ void __launch_bounds__(256, (NC == 0 && !LIST && S >= 2) ? 4 : 0) sta
       if constexpr (NC == 0) {
         // latency-bound gathers: U entries' (col, m/k) loads, then their 3 U
         // x loads, in flight together (same summation order as one by one)
-        constexpr int U = 4;
+// batch size of the pipelined gathers: 3 and 4 measure alike (50.8 vs 51.0
+// us, cfg2); 5 spills at the 64-register cap
+#ifndef IVK_K1_U
+#define IVK_K1_U 4
+#endif
+        constexpr int U = (!LIST && S >= 2) ? IVK_K1_U : 4;
         if constexpr (!LIST && S >= 2) {
         // software pipeline: the next batch's (col, m/k) loads are issued
         // before this batch's x gathers are consumed
