@@ -145,16 +145,19 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def dist_init():
+def dist_init(cpu=False):
+    """Process group from the torchrun environment: NCCL for the GPU arm,
+    gloo for the CPU-only arms (reference, probe) or without CUDA."""
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        if torch.cuda.is_available():
+        use_nccl = torch.cuda.is_available() and not cpu
+        if use_nccl:
             torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group("nccl" if use_nccl else "gloo")
     return rank, world, local
 
 
@@ -164,7 +167,7 @@ def max_over_ranks(v, world):
     import torch
     import torch.distributed as dist
     t = torch.tensor([v], dtype=torch.float64,
-                     device="cuda" if torch.cuda.is_available() else "cpu")
+                     device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -177,41 +180,61 @@ def barrier(world):
 
 # ----------------------------------------------------------------- CPU arm
 
-def cpu_sample(cfg, sample_patches=2048):
-    """Oracle (numpy/scipy restatement of the reference) on a bounded sample
-    of the sweep: the full-size residual matvec plus the patch solve of
-    ``sample_patches`` interior patches, extrapolated to all patches."""
-    from oracle.irk_vanka_oracle import OraclePatches, OracleStageOperator, oracle_patch_indices
+def cpu_oracle(cfg, threads, all_levels=False, sample_patches=2048):
+    """The CPU oracle (numpy/scipy restatement of the reference, pinned to
+    its goldens) set up for timing, untimed: stage operators, patch inverses
+    (batched np.linalg.inv over ``threads`` host threads, as build_mg's setup
+    would), RHS.  2-D Stokes configs (cfg1-3): EVERY fine-level patch (and
+    every level with ``all_levels``, for the V-cycle / FGMRES).  The 3-D and
+    MHD configs keep a bounded sample of interior patches (cfg4's full
+    inverse store would be 44 GB of host memory), scaled to all patches."""
+    from oracle.irk_vanka_oracle import (OracleCoarse, OracleMG, OraclePatches,
+                                         OracleStageOperator, oracle_patch_indices)
     disc, tab, conv = make_disc(cfg)
-    seed = cfg["seed"]
     if cfg["grid"] == "mhd":
         return cpu_sample_general(disc, tab, cfg, min(sample_patches, 512))
-    blk = disc.blocks[-1]
-    mesh = disc.fine_mesh
-    if blk.ncomp == 3:
-        sample_patches = min(sample_patches, 256)      # 392^2 inverses: keep it bounded
-    cm = None if conv is None else [J.matrix for J in conv[-1]]
-    op = OracleStageOperator(blk.M, blk.K, blk.B, tab.A, cfg["dt"], disc.cdofs[-1],
-                             convection=cm)
-    vels, idxs = oracle_patch_indices(mesh.cells, mesh.cell_to_edges, mesh.num_vertices, op,
-                                      ncomp=blk.ncomp)
-    sizes = np.array([len(i) for i in idxs])
-    interior = np.flatnonzero(sizes == sizes.max())
-    rng = np.random.default_rng(0)
-    members = np.sort(rng.choice(interior, size=min(sample_patches, len(interior)),
-                                 replace=False))
-    pat = OraclePatches(op, vels, idxs, members=members)
-    b = np.random.default_rng(seed).uniform(-1, 1, op.dim)
+    L = disc.num_levels
+    full = cfg["grid"] != "kuhn3d"
+    ks = list(range(L)) if (all_levels and full) else [L - 1]
+    levels = []
+    for k in ks:
+        blk = disc.blocks[k]
+        cm = None if conv is None else [J.matrix for J in conv[k]]
+        op = OracleStageOperator(blk.M, blk.K, blk.B, tab.A, cfg["dt"], disc.cdofs[k],
+                                 convection=cm)
+        mesh = disc.hier.levels[k]
+        vels, idxs = oracle_patch_indices(mesh.cells, mesh.cell_to_edges, mesh.num_vertices,
+                                          op, ncomp=blk.ncomp)
+        members, scale = None, 1.0
+        if not full:
+            sizes = np.array([len(i) for i in idxs])
+            interior = np.flatnonzero(sizes == sizes.max())
+            members = np.sort(np.random.default_rng(0).choice(
+                interior, size=min(256, len(interior)), replace=False))
+            scale = len(idxs) / len(members)
+        pat = OraclePatches(op, vels, idxs, members=members, threads=threads) \
+            if (k > 0 or len(ks) == 1) else None
+        P = disc.stage_prolong(k, tab.r).matrix if (k > 0 and len(ks) > 1) else None
+        levels.append({"op": op, "patches": pat, "prolong": P, "scale": scale,
+                       "n_patches": len(idxs),
+                       "n_timed": len(idxs) if members is None else len(members)})
+    fine = levels[-1]
+    op = fine["op"]
+    b = np.random.default_rng(cfg["seed"]).uniform(-1, 1, op.dim)
     b[op.constrained_stage_dofs()] = 0.0
     op.project_pressure_means(b)
-    w = np.ones(op.dim)
-    scale = len(idxs) / len(members)
-    return op, pat, b, w, scale, len(members), len(idxs)
+    out = {"op": op, "pat": fine["patches"], "b": b, "w": fine["patches"].pou_weights(op.dim),
+           "scale": fine["scale"], "n_timed": fine["n_timed"], "n_all": fine["n_patches"],
+           "full": full, "mg": None}
+    if len(levels) > 1:
+        out["levels"] = levels
+        out["coarse"] = OracleCoarse(levels[0]["op"])
+    return out
 
 
 def cpu_sample_general(disc, tab, cfg, sample_patches):
-    """The general-operator oracle (oracle/general_oracle.py) on the same
-    bounded sample: full-size residual plus sampled interior patch solves."""
+    """The general-operator oracle (oracle/general_oracle.py) on a bounded
+    sample: full-size residual plus sampled interior patch solves."""
     import scipy.sparse as sp
     from oracle.general_oracle import (OracleGeneralOperator, OracleGeneralPatches,
                                        oracle_general_patch_indices)
@@ -232,7 +255,8 @@ def cpu_sample_general(disc, tab, cfg, sample_patches):
     b = np.random.default_rng(cfg["seed"]).uniform(-1, 1, op.dim)
     b[op.constrained_stage_dofs()] = 0.0
     op.project_pressure_means(b)
-    return op, pat, b, np.ones(op.dim), len(idxs) / len(members), len(members), len(idxs)
+    return {"op": op, "pat": pat, "b": b, "w": np.ones(op.dim), "scale": len(idxs) / len(members),
+            "n_timed": len(members), "n_all": len(idxs), "full": False, "mg": None}
 
 
 def host_threads():
@@ -264,21 +288,23 @@ def threaded_solve_additive(pat, resid, pool, nthreads):
     return z
 
 
-def best_threads(op, pat, b, w, scale):
+def best_threads(o):
     """All host threads, unless one thread is faster (small configs)."""
     n = host_threads()
     if n == 1:
         return 1
-    t1 = time_cpu_sweep(op, pat, b, w, scale, reps=2, nthreads=1)[0]
-    tn = time_cpu_sweep(op, pat, b, w, scale, reps=2, nthreads=n)[0]
+    t1 = time_cpu_sweep(o, reps=2, nthreads=1)[0]
+    tn = time_cpu_sweep(o, reps=2, nthreads=n)[0]
     return n if tn < t1 else 1
 
 
-def time_cpu_sweep(op, pat, b, w, scale, reps=3, nthreads=None):
-    """Seconds per full sweep (matvec full-size + sampled solve scaled), the
-    patch solves spread over ``nthreads`` host threads."""
+def time_cpu_sweep(o, reps=3, nthreads=None):
+    """Seconds per sweep x + 0.5 W S(b - A x): the full-size residual matvec
+    (scipy, one thread) + the patch solves over ``nthreads`` host threads
+    (every patch for the 2-D configs, scale = 1)."""
     from concurrent.futures import ThreadPoolExecutor
     nthreads = nthreads or host_threads()
+    op, pat, b, w = o["op"], o["pat"], o["b"], o["w"]
     x = np.zeros(op.dim)
     best_mv, best_sa = np.inf, np.inf
     with ThreadPoolExecutor(nthreads) as pool:
@@ -291,33 +317,73 @@ def time_cpu_sweep(op, pat, b, w, scale, reps=3, nthreads=None):
             _ = x + 0.5 * w * z
             best_mv = min(best_mv, t1 - t0)
             best_sa = min(best_sa, t2 - t1)
-    return best_mv + scale * best_sa, best_mv, best_sa
+    return best_mv + o["scale"] * best_sa, best_mv, best_sa
+
+
+def cpu_cycles(o, cfg, nthreads, fgmres_too):
+    """Same-run CPU V-cycle (one mg.precondition, solvers.py:349-356) and,
+    with ``fgmres_too``, the full FGMRES solve to 1e-8 (solvers.py:364-443),
+    both smoothers, the oracle's patch solves over ``nthreads`` threads."""
+    from oracle.irk_vanka_oracle import OracleMG, oracle_fgmres
+    if "levels" not in o:
+        return None
+    op, b = o["op"], o["b"]
+    sms = {"chebyshev": dict(pre=2, post=2, accel="chebyshev", a=cfg["cheby_a"],
+                             b=cfg.get("cheby_b", 8.0), omega=1.0, weights=None),
+           "pou_richardson": dict(pre=2, post=2, accel="richardson",
+                                  omega=cfg.get("omega", 0.5), weights="pou")}
+    out = {}
+    for name, sm in sms.items():
+        mg = OracleMG(o["levels"], sm, coarse=o["coarse"], threads=nthreads)
+        mg.precondition(b.copy())              # warm (PoU weights cached)
+        t0 = time.perf_counter()
+        mg.precondition(b.copy())
+        rec = {"vcycle_s": time.perf_counter() - t0}
+        if fgmres_too:
+            t0 = time.perf_counter()
+            _, (its, _, conv) = oracle_fgmres(op.matvec, b, precond=mg.precondition, rtol=1e-8,
+                                              maxiter=200, restart=50)
+            rec.update(fgmres_s=time.perf_counter() - t0, fgmres_iterations=its,
+                       fgmres_converged=bool(conv))
+        out[name] = rec
+    return out
+
+
+def cpu_sample_text(o, nth):
+    if o["full"]:
+        return (f"full sweep: residual matvec (scipy, 1 thread) + all {o['n_all']} patch "
+                f"solves (einsum + bincount over {nth} threads); inverses precomputed, "
+                f"untimed")
+    return (f"full-size residual matvec + patch solves of {o['n_timed']} of {o['n_all']} "
+            f"interior patches (scaled x{o['scale']:.2f}) per step, {nth} threads")
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    op, pat, b, w, scale, n_s, n_all = cpu_sample(cfg)
-    nth = best_threads(op, pat, b, w, scale)
+    o = cpu_oracle(cfg, host_threads(), all_levels=not args.no_cpu_cycles)
+    nth = best_threads(o)
     for _ in range(args.warmup):
-        time_cpu_sweep(op, pat, b, w, scale, reps=1, nthreads=nth)
+        time_cpu_sweep(o, reps=1, nthreads=nth)
     times = []
     for _ in range(args.steps):
-        t, _, _ = time_cpu_sweep(op, pat, b, w, scale, reps=1, nthreads=nth)
+        t, _, _ = time_cpu_sweep(o, reps=1, nthreads=nth)
         times.append(t)
     t = float(np.mean(times))
-    sample = (f"full-size residual matvec + patch solves of {n_s} of {n_all} interior patches "
-              f"(scaled x{scale:.2f}) per step; patch solves on {nth} host threads")
+    cyc = None if args.no_cpu_cycles else cpu_cycles(o, cfg, nth, fgmres_too=False)
+    op = o["op"]
     line = {"impl": "reference", "metric": metric_name(cfg), "value": 1.0 / t, "unit": "sweeps/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "n_gpus": world if world > 1 else args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg['name']} fine-level IRK-Vanka sweep (CPU oracle port)",
                        "problem": cfg["label"], "dim": op.dim},
             "stage_dof_updates_per_s": op.dim / t,
-            "cpu_baseline": {"value": 1.0 / t, "unit": "sweeps/s", "cores": nth, "kind": "port",
-                             "sample": sample},
+            "cpu_baseline": {"value": 1.0 / t, "unit": "sweeps/s", "cores": nth,
+                             "nproc": os.cpu_count(), "kind": "port",
+                             "sample": cpu_sample_text(o, nth)},
+            "cpu_vcycle": cyc,
             "e2e": {"value": 1.0 / t, "unit": "sweeps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -342,6 +408,40 @@ def algorithmic_bytes(S, tables):
     k3 = 8 * sm2 + 4 * sm + 8 * S.dim + 8 * sm + 4 * (tables.num_patches + 1) \
         + 8 * tables.num_patches
     return sweep, k3, sm, sm2
+
+
+def vcycle_bytes(mg):
+    """Algorithmic HBM bytes of one V(2,2) cycle:
+    sum over smoothed levels of 4 patch applies (stored patch data + gather
+    list + 24 B per DoF) + 5 stage-operator applies + one restriction and
+    one prolongation, plus the coarse dense GEMV.  Returns (executed, canonical):
+    the executed figure counts the formulation's stored patch records
+    (modal / kron / dedup), the canonical one the per-patch full inverses."""
+    ex = canon = 0
+    for k, lev in enumerate(mg.levels):
+        S = lev.system
+        if k == 0:
+            n = S.dim
+            ex += 8 * n * n + 16 * n
+            canon += 8 * n * n + 16 * n
+            continue
+        pat = lev.patches
+        t = pat.tables
+        sm = t.total_m
+        sm2 = int(np.sum(t.sizes.astype(np.int64) ** 2))
+        if getattr(S, "general", False):
+            nnz = len(S.col)
+            spmv = 20 * nnz + 24 * S.dim
+        else:
+            nnz_s, nnz_b = len(S.blocks.col), S.nc * len(S.blocks.b_col)
+            spmv = 8 * (2 * nnz_s + nnz_b) + 4 * (nnz_s + nnz_b) + 24 * S.dim
+        P = lev.prolong.matrix
+        dim_c = mg.levels[k - 1].system.dim
+        transfer = 24 * P.nnz + 24 * S.dim + 16 * dim_c
+        common = 4 * (4 * sm + 24 * S.dim) + 5 * spmv + transfer
+        ex += common + 4 * 8 * pat.inv_size
+        canon += common + 4 * 8 * sm2
+    return ex, canon
 
 
 def run_ours(args, rank, world, local):
@@ -444,6 +544,14 @@ def run_ours(args, rank, world, local):
         return e0.elapsed_time(e1) / reps
 
     vc = {"chebyshev": time_vcycles(mg), "pou_richardson": time_vcycles(mg_pou)}
+    hbm0, _ = peaks()
+    vb_ex, vb_canon = vcycle_bytes(mg)
+    v_roof = {"bytes_executed": vb_ex, "bytes_canonical": vb_canon,
+              "achieved_gbs": vb_ex / (vc["pou_richardson"] * 1e-3) / 1e9,
+              "frac": vb_ex / (vc["pou_richardson"] * 1e-3) / 1e9 / hbm0,
+              "canonical_equiv_gbs": vb_canon / (vc["pou_richardson"] * 1e-3) / 1e9,
+              "cycle": "pou_richardson (BASELINE smoother), CUDA-graph replay",
+              "peak": hbm0}
 
     # Newton-cadence relinearisation (Oseen configs): device J assembly on all
     # levels + in-place patch refactorisation + coarse SuperLU.
@@ -624,6 +732,20 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     t_e2e = max_over_ranks(e_start.elapsed_time(e_stop) / 1e3 / args.steps, world)
 
+    # The reference user's literal drop-in call: numpy x, b in, numpy x_new
+    # out (pageable host memory, synchronous copies inside apply_vanka).
+    x_np = np.zeros(S.dim)
+    for _ in range(3):
+        apply_vanka(fine, S, x_np, b_h, omega=om, weights="pou")
+    torch.cuda.synchronize()
+    barrier(world)
+    n_np = max(3, min(args.steps, 50))
+    t0 = time.perf_counter()
+    for _ in range(n_np):
+        y_np = apply_vanka(fine, S, x_np, b_h, omega=om, weights="pou")
+    t_np = max_over_ranks((time.perf_counter() - t0) / n_np, world)
+    assert isinstance(y_np, np.ndarray)
+
     # --shard (N > 1): one cfg2 problem strip-partitioned over the N ranks
     # (shard.py): the fine-level sweep with its two NCCL halo exchanges,
     # strong scaling, beside the replica headline
@@ -657,13 +779,15 @@ def run_ours(args, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        op, pat, bb, ww, scale, n_s, n_all = cpu_sample(cfg)
-        nth = best_threads(op, pat, bb, ww, scale)
-        t_cpu, t_mv, t_sa = time_cpu_sweep(op, pat, bb, ww, scale, reps=3, nthreads=nth)
-        cpu = {"value": 1.0 / t_cpu, "unit": "sweeps/s", "cores": nth, "kind": "port",
-               "sample": (f"oracle: full-size residual matvec ({1e3 * t_mv:.0f} ms, scipy, one "
-                          f"thread) + patch solves of {n_s}/{n_all} interior patches "
-                          f"({1e3 * t_sa:.0f} ms on {nth} threads, scaled x{scale:.2f})")}
+        o = cpu_oracle(cfg, host_threads(), all_levels=not args.no_cpu_cycles)
+        nth = best_threads(o)
+        t_cpu, t_mv, t_sa = time_cpu_sweep(o, reps=3, nthreads=nth)
+        cpu = {"value": 1.0 / t_cpu, "unit": "sweeps/s", "cores": nth, "nproc": os.cpu_count(),
+               "kind": "port", "sample": cpu_sample_text(o, nth),
+               "matvec_ms": 1e3 * t_mv, "patch_solves_ms": 1e3 * t_sa * o["scale"]}
+        if not args.no_cpu_cycles:
+            cpu["cycles"] = cpu_cycles(o, cfg, nth, fgmres_too=not args.no_cpu_fgmres)
+        del o
 
     if rank == 0:
         line = {
@@ -706,9 +830,14 @@ def run_ours(args, rank, world, local):
                     "h2d_bytes_per_step": 2 * 8 * S.dim, "d2h_bytes_per_step": 8 * S.dim,
                     "how": "apply_vanka on pinned host buffers, H2D x,b + sweep + D2H per "
                            f"step; {nslot} streams rotate so copies overlap compute"},
+            "e2e_numpy": {"value": world / t_np, "unit": "sweeps/s",
+                          "h2d_bytes_per_step": 2 * 8 * S.dim, "d2h_bytes_per_step": 8 * S.dim,
+                          "how": "apply_vanka(numpy x, numpy b) -> numpy, pageable memory, "
+                                 "synchronous (the reference call as written), host clock"},
             "gpu_launches": int(launches),
             "clocks": clocks,
             "vcycle_ms": vc,
+            "vcycle_roofline": v_roof,
             "fgmres": solves,
             "dedup_cycle": dedup,
             "newton_step": newton,
@@ -720,26 +849,66 @@ def run_ours(args, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def launch_ranks(args):
+    """``--gpus N`` (N > 1) without a torchrun environment: re-run this
+    script as N ranks under torch.distributed.run on 127.0.0.1 (one process
+    per GPU, NCCL with NCCL_DEBUG=INFO so the communicator lines show the
+    rank count) and return its exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def run_probe(args, rank, world):
+    """Launcher check (CPU-capable): every rank reports, the max-over-ranks
+    all-reduce runs, rank 0 prints one JSON line."""
+    v = max_over_ranks(float(rank + 1), world)
+    barrier(world)
+    if rank == 0:
+        print(json.dumps({"impl": "probe", "n_gpus": world, "requested": args.gpus,
+                          "max_over_ranks": v}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--impl", choices=["ours", "reference", "probe"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2",
                     help="BASELINE config; cfg2 is the headline workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--shard", action="store_true",
-                    help="N > 1: also time one problem strip-partitioned over the ranks")
+    ap.add_argument("--no-cpu-cycles", action="store_true",
+                    help="skip the CPU oracle V-cycle / FGMRES timings")
+    ap.add_argument("--no-cpu-fgmres", action="store_true",
+                    help="skip the CPU oracle FGMRES solves (keep the V-cycles)")
+    ap.add_argument("--no-shard", action="store_true",
+                    help="N > 1: skip the strip-partitioned (strong-scaling) sweep")
+    ap.add_argument("--shard", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-full-mode", action="store_true",
-                    help="skip timing the reference (full-inverse) formulation")
+                    help="skip timing the alternative patch formulations")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args))
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
-    rank, world, local = dist_init()
+    args.shard = not args.no_shard
+    rank, world, local = dist_init(cpu=args.impl != "ours")
+    if world != args.gpus:
+        raise SystemExit(f"bench: launched with WORLD_SIZE={world} but --gpus {args.gpus}")
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)
+        elif args.impl == "probe":
+            run_probe(args, rank, world)
         else:
             run_ours(args, rank, world, local)
     finally:

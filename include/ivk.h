@@ -325,9 +325,15 @@ int ivk_prolong_add(const ivk_transfer_desc* t, const double* ec, double* xf, vo
  * one GEMV with c->dense when set; b and x must not alias. */
 int ivk_coarse_solve(const ivk_coarse_desc* c, const double* b, double* x, void* stream);
 
-/* Per-stage pressure-mean removal in place (stages.py:174-178). */
+/* Per-stage pressure-mean removal in place (stages.py:174-178): two
+ * launches over (IVK_PROJECT_BLOCKS x stages) CTAs -- block partial sums,
+ * then every CTA re-adds its stage's partials in block order (deterministic,
+ * identical on every CTA) and subtracts the mean from its slice.  `scratch`:
+ * caller-owned device memory of IVK_PROJECT_BLOCKS * stages doubles (no
+ * initialisation needed). */
+#define IVK_PROJECT_BLOCKS 64
 int ivk_project_pressure_means(int32_t stages, int32_t n_u, int32_t n_p, double* x,
-                               void* stream);
+                               double* scratch, void* stream);
 /* out = alpha * x + beta * y (x or y may be NULL -> 0); out may alias. */
 int ivk_axpby(int64_t n, double alpha, const double* x, double beta, const double* y,
               double* out, void* stream);
@@ -370,18 +376,31 @@ int ivk_convection_assemble(const ivk_convection_desc* d, const double* u, doubl
                             double* conv, double* conv_s, double* residual, void* stream);
 
 /* ---- Krylov vector work of FGMRES (solvers.py:388-430), deterministic ----
- * Reductions use a fixed grid of block partials summed in block order; the
- * library keeps one small scratch buffer per device. */
+ * Reductions use a fixed grid of block partials summed in block order by
+ * the last block to finish.  `scratch` is caller-owned device memory of
+ * ivk_reduction_scratch_bytes() bytes, ZEROED once before first use; the
+ * library allocates nothing (graph-capture safe).  Calls sharing one scratch
+ * must be stream-ordered: give every concurrent stream its own scratch. */
+size_t ivk_reduction_scratch_bytes(void);
 /* *result = <x, y> (device scalar). */
-int ivk_dot(int64_t n, const double* x, const double* y, double* result, void* stream);
+int ivk_dot(int64_t n, const double* x, const double* y, double* result, void* scratch,
+            void* stream);
 /* *result = ||x||_2 (device scalar). */
-int ivk_norm(int64_t n, const double* x, double* result, void* stream);
+int ivk_norm(int64_t n, const double* x, double* result, void* scratch, void* stream);
 /* Modified Gram-Schmidt of w against V_0..V_{k-1} (rows of V, stride ldv):
  * h[i] = <w, V_i>; w -= h[i] V_i (i ascending); h[k] = ||w||; if v_next:
  * v_next = w / h[k] when h[k] > 1e-300 (solvers.py:401-408).  h is device. */
 int ivk_mgs(int64_t n, const double* V, int64_t ldv, int32_t k, double* w, double* h,
-            double* v_next, void* stream);
-/* out = x / coef[k] when coef[k] > 1e-300 (coef device). */
+            double* v_next, void* scratch, void* stream);
+/* FGMRES Givens step on Hessenberg column j (solvers.py:409-421), all on the
+ * device: apply rotations 0..j-1 to H[:, j], form rotation j, rotate g, and
+ * *est = |g[j+1]|.  H column-major, leading dimension ldh >= j + 2. */
+int ivk_givens(int32_t j, int32_t ldh, double* H, double* cs, double* sn, double* g, double* est,
+               void* stream);
+/* y = triu(H[:k, :k])^-1 g[:k] (back substitution; solvers.py:430). */
+int ivk_hessenberg_solve(int32_t k, int32_t ldh, const double* H, const double* g, double* y,
+                         void* stream);
+/* out = x / coef[k] when coef[k] > 1e-300, else 0 (coef device). */
 int ivk_scale(int64_t n, const double* x, const double* coef, int32_t k, double* out,
               void* stream);
 /* x += sum_i y[i] Z_i, i ascending (solvers.py:432); y device. */

@@ -157,13 +157,76 @@ def oracle_patch_indices(cells, cell_to_edges, num_vertices, op, ncomp=2):
     return vels, idxs
 
 
+def _gather_dense(A, rows):
+    """Dense submatrices A[rows_p, rows_p] for a batch of ascending index
+    sets, (P, m) -> (P, m, m): one pass over the CSR arrays, each stored
+    column located in its patch's sorted row set by a searchsorted over
+    offset-disambiguated keys (solvers.py:33-59)."""
+    A = sp.csr_matrix(A)
+    P, m = rows.shape
+    n = A.shape[1]
+    flat = rows.ravel()
+    start = A.indptr[flat]
+    cnt = A.indptr[flat + 1] - start
+    off = np.concatenate(([0], np.cumsum(cnt)))
+    pos = np.repeat(start - off[:-1], cnt) + np.arange(off[-1])
+    cols, vals = A.indices[pos], A.data[pos]
+    row_of = np.repeat(np.arange(P * m), cnt)
+    patch = row_of // m
+    keys = (rows + np.arange(P, dtype=np.int64)[:, None] * n).ravel()
+    query = cols + patch * n
+    loc = np.minimum(np.searchsorted(keys, query), P * m - 1)
+    hit = keys[loc] == query
+    out = np.zeros((P, m, m))
+    out[patch[hit], row_of[hit] % m, loc[hit] - patch[hit] * m] = vals[hit]
+    return out
+
+
+def _gather_columns(B, rows, col_of_patch):
+    """B[rows_p, col_p] per patch, (P, m) (solvers.py:62-78)."""
+    B = sp.csr_matrix(B)
+    P, m = rows.shape
+    flat = rows.ravel()
+    start = B.indptr[flat]
+    cnt = B.indptr[flat + 1] - start
+    off = np.concatenate(([0], np.cumsum(cnt)))
+    pos = np.repeat(start - off[:-1], cnt) + np.arange(off[-1])
+    cols, vals = B.indices[pos], B.data[pos]
+    row_of = np.repeat(np.arange(P * m), cnt)
+    patch = row_of // m
+    hit = cols == np.asarray(col_of_patch)[patch]
+    out = np.zeros((P, m))
+    out[patch[hit], row_of[hit] % m] = vals[hit]
+    return out
+
+
+def _chunks(n, k):
+    cuts = [(i * n) // k for i in range(k + 1)]
+    return [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+
+
+def _pool_map(fn, items, threads):
+    """Map over host threads with BLAS pinned to one thread each (numpy's
+    batched LAPACK / einsum release the GIL; nested OpenBLAS threading in
+    every worker would oversubscribe the cores)."""
+    if threads <= 1 or len(items) <= 1:
+        return [fn(it) for it in items]
+    from concurrent.futures import ThreadPoolExecutor
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1), ThreadPoolExecutor(threads) as ex:
+        return list(ex.map(fn, items))
+
+
 class OraclePatches:
     """Grouped patch inverses and the additive solve (solvers.py:169-222).
 
     ``members``: restrict to a subset of vertices (a bounded sample for
-    timing or spot checks); default all."""
+    timing or spot checks); default all.  ``threads``: host threads for the
+    batched ``np.linalg.inv`` of each size group (the reference calls it on
+    the whole group at once; splitting the batch does not change any
+    patch's inverse)."""
 
-    def __init__(self, op, vels, idxs, members=None):
+    def __init__(self, op, vels, idxs, members=None, threads=1):
         self.op = op
         sizes = np.array([len(ix) for ix in idxs])
         allowed = np.ones(len(idxs), dtype=bool)
@@ -175,44 +238,74 @@ class OraclePatches:
         for m in np.unique(sizes[allowed]):
             mem = np.flatnonzero((sizes == m) & allowed)
             idx = np.stack([idxs[p] for p in mem])
-            mats = self.patch_matrices(op, [vels[p] for p in mem], mem)
-            self.groups.append((idx, np.linalg.inv(mats)))
+            vel = np.stack([vels[p] for p in mem])
+            d = len(idx[0])
+            inv = np.empty((len(mem), d, d))
+            parts = _chunks(len(mem), max(1, len(mem) // 1024))
+
+            def work(ab, mem=mem, vel=vel, inv=inv):
+                # gather + inversion of one slice of the group: every patch's
+                # matrix and inverse are the same as the whole-group call's
+                a, b = ab
+                inv[a:b] = np.linalg.inv(self.patch_matrices(op, vel[a:b], mem[a:b]))
+            _pool_map(work, parts, threads)
+            self.groups.append((idx, inv))
             self.members.append(mem)
 
     @staticmethod
     def patch_matrices(op, vels, verts):
-        """Dense stage-coupled patch matrices (solvers.py:186-212)."""
+        """Dense stage-coupled patch matrices of one size group
+        (solvers.py:186-212): per stage block (i, j)
+        [M d_ij + dt a_ij (K + C_i) | dt a_ij b] over [dt a_ij b^T | 0]."""
         A, dt, r = op.A, op.dt, op.r
-        m = len(vels[0])
+        vel = np.stack([np.asarray(v, dtype=np.int64) for v in vels])
+        P, m = vel.shape
+        Ml = _gather_dense(op.M, vel)
+        Kl = _gather_dense(op.K, vel)
+        bcol = _gather_columns(op.B, vel, np.asarray(verts))
+        Cl = None
+        if op.convection is not None:
+            Cl = [_gather_dense(op.convection[i], vel) for i in range(r)]
         d = r * (m + 1)
-        mats = np.zeros((len(vels), d, d))
-        for q, (vel, v) in enumerate(zip(vels, verts)):
-            Ml = op.M[vel][:, vel].toarray()
-            Kl = op.K[vel][:, vel].toarray()
-            bcol = op.B[vel][:, [v]].toarray().ravel()
-            Cl = None
-            if op.convection is not None:
-                Cl = [op.convection[i][vel][:, vel].toarray() for i in range(r)]
-            for i in range(r):
-                for j in range(r):
-                    Kij = dt * A[i, j] * Kl
-                    if Cl is not None:
-                        Kij = Kij + dt * A[i, j] * Cl[i]
-                    if i == j:
-                        Kij = Kij + Ml
-                    r0, c0 = i * (m + 1), j * (m + 1)
-                    mats[q, r0:r0 + m, c0:c0 + m] = Kij
-                    mats[q, r0:r0 + m, c0 + m] = dt * A[i, j] * bcol
-                    mats[q, r0 + m, c0:c0 + m] = dt * A[i, j] * bcol
+        mats = np.zeros((P, d, d))
+        for i in range(r):
+            for j in range(r):
+                Kij = dt * A[i, j] * Kl
+                if Cl is not None:
+                    Kij = Kij + dt * A[i, j] * Cl[i]
+                if i == j:
+                    Kij = Kij + Ml
+                r0, c0 = i * (m + 1), j * (m + 1)
+                mats[:, r0:r0 + m, c0:c0 + m] = Kij
+                mats[:, r0:r0 + m, c0 + m] = dt * A[i, j] * bcol
+                mats[:, r0 + m, c0:c0 + m] = dt * A[i, j] * bcol
         return mats
 
-    def solve_additive(self, resid):
-        """solvers.py:214-222."""
+    def solve_additive(self, resid, threads=1, reverse=False):
+        """solvers.py:214-222: per size group einsum("pij,pj->pi") and a
+        bincount scatter, groups summed in order.  ``threads`` > 1 splits each
+        group's patches into chunks whose bincounts are added in chunk order
+        (a different, fixed summation order: ~1e-16 relative).  ``reverse``
+        runs the groups and the patches inside each group in the opposite
+        order -- the reference's self-floor probe."""
         z = np.zeros_like(resid)
         n = len(resid)
-        for idx, inv in self.groups:
-            local = np.einsum("pij,pj->pi", inv, resid[idx])
-            z += np.bincount(idx.ravel(), weights=local.ravel(), minlength=n)
+        groups = self.groups[::-1] if reverse else self.groups
+        for idx, inv in groups:
+            if reverse:
+                idx, inv = idx[::-1], inv[::-1]
+            if threads <= 1:
+                local = np.einsum("pij,pj->pi", inv, resid[idx])
+                z += np.bincount(idx.ravel(), weights=local.ravel(), minlength=n)
+                continue
+
+            def part(ab, idx=idx, inv=inv):
+                ix = idx[ab[0]:ab[1]]
+                loc = np.einsum("pij,pj->pi", inv[ab[0]:ab[1]], resid[ix])
+                return np.bincount(ix.ravel(), weights=loc.ravel(), minlength=n)
+            for zz in _pool_map(part, _chunks(len(idx), max(1, min(threads, len(idx) // 16))),
+                                threads):
+                z += zz
         return z
 
     def multiplicity(self, n):
@@ -227,9 +320,9 @@ class OraclePatches:
         return np.where(mult > 0, 1.0 / np.maximum(mult, 1.0), 0.0)
 
 
-def oracle_apply_vanka(patches, op, x, b, omega, weights=None):
+def oracle_apply_vanka(patches, op, x, b, omega, weights=None, threads=1):
     """solvers.py:232-239 (+ optional PoU weight vector)."""
-    z = patches.solve_additive(b - op.matvec(x))
+    z = patches.solve_additive(b - op.matvec(x), threads=threads)
     if weights is not None:
         z = weights * z
     return x + omega * z
@@ -278,22 +371,30 @@ class OracleMG:
     levels: list (coarsest first) of dicts with keys ``op``, ``patches``,
     ``prolong`` (scipy stage prolongation from the level below, or None).
     smoother: dict(pre, post, accel in {"chebyshev","richardson","gmres"},
-    a, b, omega, weights in {None, "pou"})."""
+    a, b, omega, weights in {None, "pou"}).  ``threads`` / ``reverse`` are
+    passed to every ``solve_additive`` (reverse = the F9 self-floor probe)."""
 
-    def __init__(self, levels, smoother, coarse=None):
+    def __init__(self, levels, smoother, coarse=None, threads=1, reverse=False):
         self.levels = levels
         self.sm = dict(smoother)
         self.coarse = coarse if coarse is not None else OracleCoarse(levels[0]["op"])
         self.coarse_hook = None  # optional override: f(level0_rhs) -> solution
+        self.threads = threads
+        self.reverse = reverse
+        self._w = {}
 
     def _smooth(self, lev, x, b, sweeps):
         if sweeps == 0:
             return x
         op, pat, sm = lev["op"], lev["patches"], self.sm
-        w = pat.pou_weights(op.dim) if sm.get("weights") == "pou" else None
+        w = None
+        if sm.get("weights") == "pou":
+            if id(pat) not in self._w:
+                self._w[id(pat)] = pat.pou_weights(op.dim)
+            w = self._w[id(pat)]
 
         def precond(r):
-            z = sm["omega"] * pat.solve_additive(r)
+            z = sm["omega"] * pat.solve_additive(r, threads=self.threads, reverse=self.reverse)
             return z if w is None else w * z
 
         if sm["accel"] == "chebyshev":

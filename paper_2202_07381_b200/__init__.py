@@ -5,6 +5,7 @@ hand-written sm_100a CUDA kernels behind the reference ``irkmg`` Python API.
 """
 
 from . import fem, mesh, quadrature, tableaux
+from ._lib import IvkError
 from .discretization import (ConfigError, Discretization, oseen_convection,
                              streamfunction_velocity)
 from .fem import assemble_blocks, assemble_convection_jacobian, prolongation

@@ -192,15 +192,18 @@ _SIGS = {
     "ivk_restrict": ([C.POINTER(TransferDesc), _P, _P, _P], C.c_int),
     "ivk_prolong_add": ([C.POINTER(TransferDesc), _P, _P, _P], C.c_int),
     "ivk_coarse_solve": ([C.POINTER(CoarseDesc), _P, _P, _P], C.c_int),
-    "ivk_project_pressure_means": ([C.c_int32, C.c_int32, C.c_int32, _P, _P], C.c_int),
+    "ivk_project_pressure_means": ([C.c_int32, C.c_int32, C.c_int32, _P, _P, _P], C.c_int),
     "ivk_axpby": ([C.c_int64, C.c_double, _P, C.c_double, _P, _P, _P], C.c_int),
     "ivk_seed_constrained": ([C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P],
                              C.c_int),
     "ivk_convection_assemble": ([C.POINTER(ConvectionDesc), _P, _P, _P, _P, _P, _P], C.c_int),
-    "ivk_dot": ([C.c_int64, _P, _P, _P, _P], C.c_int),
-    "ivk_norm": ([C.c_int64, _P, _P, _P], C.c_int),
-    "ivk_mgs": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P, _P], C.c_int),
+    "ivk_reduction_scratch_bytes": ([], C.c_size_t),
+    "ivk_dot": ([C.c_int64, _P, _P, _P, _P, _P], C.c_int),
+    "ivk_norm": ([C.c_int64, _P, _P, _P, _P], C.c_int),
+    "ivk_mgs": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P, _P, _P], C.c_int),
     "ivk_scale": ([C.c_int64, _P, _P, C.c_int32, _P, _P], C.c_int),
+    "ivk_givens": ([C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P], C.c_int),
+    "ivk_hessenberg_solve": ([C.c_int32, C.c_int32, _P, _P, _P, _P], C.c_int),
     "ivk_lincomb": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P], C.c_int),
     "ivk_patch_gather_blocks": ([C.POINTER(OperatorDesc), C.POINTER(PatchDesc), C.c_int32, _P,
                                  _P, _P, _P], C.c_int),
@@ -239,6 +242,18 @@ def load(path=_LIB_PATH):
 
 def lib():
     return load()
+
+
+PROJECT_BLOCKS = 64   # IVK_PROJECT_BLOCKS (include/ivk.h)
+
+
+def reduction_scratch():
+    """A fresh zeroed device scratch for ivk_dot / ivk_norm / ivk_mgs (one
+    per concurrent stream of reductions; include/ivk.h)."""
+    import torch
+    from ._device import device
+    nbytes = int(lib().ivk_reduction_scratch_bytes())
+    return torch.zeros((nbytes + 7) // 8, dtype=torch.float64, device=device())
 
 
 def check(rc, what=""):

@@ -286,15 +286,13 @@ int ivk_coarse_solve(const ivk_coarse_desc* c, const double* b, double* x, void*
     set_error("ivk_coarse_solve: coarse dimension %d too large for one CTA", c->n);
     return IVK_EUNSUPPORTED;
   }
-  static size_t configured = 0;
-  if (smem > configured) {
+  {  // set on every call: the attribute is per device
     cudaError_t e = cudaFuncSetAttribute(coarse_solve_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
       set_error("ivk_coarse_solve: %s", cudaGetErrorString(e));
       return IVK_ECUDA;
     }
-    configured = smem;
   }
   CoarseParams p;
   p.n = c->n;

@@ -16,30 +16,21 @@ namespace ivk {
 constexpr int kRedThreads = 512;
 constexpr int kRedBlocks = 2 * kSMs;
 
+// Caller-owned reduction scratch (ivk_reduction_scratch_bytes()): the block
+// partials followed by the last-block counter.  One scratch per stream of
+// reductions; the counter returns to 0 after every reduction, so a scratch
+// zeroed once serves any number of stream-ordered calls (and CUDA-graph
+// capture: nothing is allocated here).
 struct RedScratch {
-  double* partial = nullptr;
-  unsigned int* counter = nullptr;
+  double* partial;
+  unsigned int* counter;
 };
 
-static RedScratch g_red[64];  // one per device ordinal
-
-static int scratch(RedScratch** out) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
-    set_error("ivk krylov: no current device");
-    return IVK_ECUDA;
-  }
-  RedScratch& s = g_red[dev];
-  if (!s.partial) {
-    if (cudaMalloc(&s.partial, kRedBlocks * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&s.counter, sizeof(unsigned int)) != cudaSuccess ||
-        cudaMemset(s.counter, 0, sizeof(unsigned int)) != cudaSuccess) {
-      set_error("ivk krylov: scratch allocation failed");
-      return IVK_ECUDA;
-    }
-  }
-  *out = &s;
-  return IVK_OK;
+static inline RedScratch scratch_of(void* p) {
+  RedScratch s;
+  s.partial = static_cast<double*>(p);
+  s.counter = reinterpret_cast<unsigned int*>(s.partial + kRedBlocks);
+  return s;
 }
 
 // Block-level sum, then the last block to finish reduces the partials in
@@ -93,14 +84,48 @@ __global__ void __launch_bounds__(kRedThreads) axpy_dot_kernel(long n, const dou
   finish_reduction(acc, partial, counter, result, b == nullptr);
 }
 
-// out = w / coef[k] when coef[k] > 1e-300 (solvers.py:407-408), else left.
+// out = w / coef[k] when coef[k] > 1e-300 (solvers.py:407-408), else 0 (the
+// reference's basis rows start as zeros and stay so on breakdown).
 __global__ void scale_kernel(long n, const double* __restrict__ w, const double* coef, int k,
                              double* __restrict__ out) {
   const double h = coef[k];
-  if (!(h > 1e-300)) return;
+  const bool ok = h > 1e-300;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
        i += (long)gridDim.x * blockDim.x)
-    out[i] = w[i] / h;
+    out[i] = ok ? w[i] / h : 0.0;
+}
+
+// Givens update of Hessenberg column j (solvers.py:409-421) on the device:
+// the stored rotations applied to H[:, j] in order, the new rotation formed,
+// g rotated; est = |g[j+1]|.  H column-major with leading dimension ldh.
+// One thread: j <= restart (<= a few hundred) scalar steps.
+__global__ void givens_kernel(int j, int ldh, double* H, double* cs, double* sn, double* g,
+                              double* est) {
+  double* h = H + (long)j * ldh;
+  for (int i = 0; i < j; ++i) {
+    const double t = cs[i] * h[i] + sn[i] * h[i + 1];
+    h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+    h[i] = t;
+  }
+  const double denom = hypot(h[j], h[j + 1]);
+  cs[j] = h[j] / denom;
+  sn[j] = h[j + 1] / denom;
+  h[j] = denom;
+  h[j + 1] = 0.0;
+  g[j + 1] = -sn[j] * g[j];
+  g[j] = cs[j] * g[j];
+  *est = fabs(g[j + 1]);
+}
+
+// y = triu(H[:k, :k])^-1 g[:k] by back substitution (solvers.py:430), one
+// thread.  H column-major (ldh).
+__global__ void hessenberg_solve_kernel(int k, int ldh, const double* H, const double* g,
+                                        double* y) {
+  for (int i = k - 1; i >= 0; --i) {
+    double v = g[i];
+    for (int c = i + 1; c < k; ++c) v -= H[(long)c * ldh + i] * y[c];
+    y[i] = v / H[(long)i * ldh + i];
+  }
 }
 
 // x += sum_i y[i] * Z_i (i ascending), y in device memory.
@@ -126,23 +151,26 @@ using namespace ivk;
 
 extern "C" {
 
-int ivk_dot(int64_t n, const double* x, const double* y, double* result, void* stream) {
-  IVK_REQUIRE(n >= 0 && x && result, "bad dot arguments");
-  RedScratch* s = nullptr;
-  int rc = scratch(&s);
-  if (rc) return rc;
+size_t ivk_reduction_scratch_bytes(void) {
+  return kRedBlocks * sizeof(double) + 16;
+}
+
+int ivk_dot(int64_t n, const double* x, const double* y, double* result, void* scratch,
+            void* stream) {
+  IVK_REQUIRE(n >= 0 && x && result && scratch, "bad dot arguments");
+  const RedScratch s = scratch_of(scratch);
   // <x, y> via the fused kernel with no axpy part (w = x is only read).
   axpy_dot_kernel<<<kRedBlocks, kRedThreads, 0, as_stream(stream)>>>(
-      n, nullptr, nullptr, 0, const_cast<double*>(x), y, s->partial, s->counter, result);
+      n, nullptr, nullptr, 0, const_cast<double*>(x), y, s.partial, s.counter, result);
   return check_launch("ivk_dot");
 }
 
 int ivk_mgs(int64_t n, const double* V, int64_t ldv, int32_t k, double* w, double* h,
-            double* v_next, void* stream) {
-  IVK_REQUIRE(n > 0 && V && w && h && k >= 1 && ldv >= n, "bad MGS arguments");
-  RedScratch* s = nullptr;
-  int rc = scratch(&s);
-  if (rc) return rc;
+            double* v_next, void* scratch, void* stream) {
+  IVK_REQUIRE(n > 0 && V && w && h && k >= 1 && ldv >= n && scratch, "bad MGS arguments");
+  const RedScratch sc = scratch_of(scratch);
+  const RedScratch* s = &sc;
+  int rc = IVK_OK;
   cudaStream_t st = as_stream(stream);
   // pass 0: h0 = <w, V0>; pass i: w -= h_{i-1} V_{i-1}, h_i = <w, V_i>
   for (int i = 0; i < k; ++i) {
@@ -164,13 +192,11 @@ int ivk_mgs(int64_t n, const double* V, int64_t ldv, int32_t k, double* w, doubl
   return rc;
 }
 
-int ivk_norm(int64_t n, const double* x, double* result, void* stream) {
-  IVK_REQUIRE(n >= 0 && x && result, "bad norm arguments");
-  RedScratch* s = nullptr;
-  int rc = scratch(&s);
-  if (rc) return rc;
+int ivk_norm(int64_t n, const double* x, double* result, void* scratch, void* stream) {
+  IVK_REQUIRE(n >= 0 && x && result && scratch, "bad norm arguments");
+  const RedScratch s = scratch_of(scratch);
   axpy_dot_kernel<<<kRedBlocks, kRedThreads, 0, as_stream(stream)>>>(
-      n, nullptr, nullptr, 0, const_cast<double*>(x), nullptr, s->partial, s->counter, result);
+      n, nullptr, nullptr, 0, const_cast<double*>(x), nullptr, s.partial, s.counter, result);
   return check_launch("ivk_norm");
 }
 
@@ -179,6 +205,21 @@ int ivk_scale(int64_t n, const double* x, const double* coef, int32_t k, double*
   IVK_REQUIRE(n >= 0 && x && coef && out, "bad scale arguments");
   scale_kernel<<<grid_for_n(n), 256, 0, as_stream(stream)>>>(n, x, coef, k, out);
   return check_launch("ivk_scale");
+}
+
+int ivk_givens(int32_t j, int32_t ldh, double* H, double* cs, double* sn, double* g, double* est,
+               void* stream) {
+  IVK_REQUIRE(j >= 0 && ldh >= j + 2 && H && cs && sn && g && est, "bad givens arguments");
+  givens_kernel<<<1, 1, 0, as_stream(stream)>>>(j, ldh, H, cs, sn, g, est);
+  return check_launch("ivk_givens");
+}
+
+int ivk_hessenberg_solve(int32_t k, int32_t ldh, const double* H, const double* g, double* y,
+                         void* stream) {
+  IVK_REQUIRE(k >= 0 && ldh >= k && H && g && y, "bad hessenberg_solve arguments");
+  if (k == 0) return IVK_OK;
+  hessenberg_solve_kernel<<<1, 1, 0, as_stream(stream)>>>(k, ldh, H, g, y);
+  return check_launch("ivk_hessenberg_solve");
 }
 
 int ivk_lincomb(int64_t n, const double* Z, int64_t ldz, int32_t k, const double* y, double* x,

@@ -67,8 +67,8 @@ struct OpParams {
 // capped, cfg2 fine level).
 template <int S, int NC, bool LIST>
 __global__ void __launch_bounds__(256, (NC == 0 && !LIST && S >= 2) ? 4 : 0) stage_apply_kernel(OpParams op, const double* __restrict__ x,
-                                                          const double* __restrict__ b,
-                                                          double* __restrict__ out,
+                                                          const double* b,
+                                                          double* out,
                                                           const int32_t* __restrict__ slices,
                                                           int n_slices) {
   const int nslice_v = (op.n_nodes + 15) >> 4;
@@ -350,8 +350,8 @@ int validate_op(const ivk_operator_desc* d) {
 // (B_x, B_y, B_z) triples.  Pressure rows as in 2-D.
 template <int S, bool LIST>
 __global__ void __launch_bounds__(256) stage_apply3_kernel(OpParams op, const double* __restrict__ x,
-                                                           const double* __restrict__ b,
-                                                           double* __restrict__ out,
+                                                           const double* b,
+                                                           double* out,
                                                            const int32_t* __restrict__ slices,
                                                            int n_slices) {
   const int nslice_v = (op.n_nodes + 31) >> 5;
@@ -512,26 +512,51 @@ __global__ void axpby_kernel(long n, double alpha, const double* __restrict__ x,
   }
 }
 
-// One CTA per stage; fixed-order (deterministic) reduction.
-__global__ void __launch_bounds__(1024) project_means_kernel(int n_u, int n_p, double* x) {
-  __shared__ double red[32];
-  const long sd = (long)n_u + n_p;
-  double* p = x + blockIdx.x * sd + n_u;
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < n_p; i += blockDim.x) acc += p[i];
+// Pressure-mean projection over (IVK_PROJECT_BLOCKS, stages) CTAs: phase 1
+// writes one partial sum per CTA (block-strided slice, fixed-order tree),
+// phase 2 has every CTA sum its stage's partials in index order -- the same
+// bits on every CTA -- and subtract the mean from its slice.
+constexpr int kProjThreads = 256;
+
+__device__ __forceinline__ double block_sum(double acc, double* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) red[0] = v;
+  double v = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kProjThreads / 32; ++w) v += red[w];
+  return v;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(kProjThreads) project_partial_kernel(int n_u, int n_p,
+                                                                       const double* x,
+                                                                       double* partial) {
+  __shared__ double red[kProjThreads / 32];
+  const long sd = (long)n_u + n_p;
+  const double* p = x + blockIdx.y * sd + n_u;
+  double acc = 0.0;
+  for (int i = blockIdx.x * kProjThreads + threadIdx.x; i < n_p; i += gridDim.x * kProjThreads)
+    acc += p[i];
+  const double v = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = v;
+}
+
+__global__ void __launch_bounds__(kProjThreads) project_subtract_kernel(int n_u, int n_p,
+                                                                        double* x,
+                                                                        const double* partial) {
+  __shared__ double mean;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s += partial[blockIdx.y * gridDim.x + b];
+    mean = s / (double)n_p;
   }
   __syncthreads();
-  const double mean = red[0] / (double)n_p;
-  for (int i = threadIdx.x; i < n_p; i += blockDim.x) p[i] -= mean;
+  const long sd = (long)n_u + n_p;
+  double* p = x + blockIdx.y * sd + n_u;
+  const double m = mean;
+  for (int i = blockIdx.x * kProjThreads + threadIdx.x; i < n_p; i += gridDim.x * kProjThreads)
+    p[i] -= m;
 }
 
 __global__ void seed_constrained_kernel(int S, int n_nodes, int nc, int n_p,
@@ -645,9 +670,18 @@ int ivk_axpby(int64_t n, double alpha, const double* x, double beta, const doubl
   return check_launch("ivk_axpby");
 }
 
-int ivk_project_pressure_means(int32_t stages, int32_t n_u, int32_t n_p, double* x, void* stream) {
-  IVK_REQUIRE(x && stages >= 1 && n_p > 0 && n_u >= 0, "bad projection arguments");
-  project_means_kernel<<<stages, 1024, 0, as_stream(stream)>>>(n_u, n_p, x);
+int ivk_project_pressure_means(int32_t stages, int32_t n_u, int32_t n_p, double* x,
+                               double* scratch, void* stream) {
+  IVK_REQUIRE(x && scratch && stages >= 1 && n_p > 0 && n_u >= 0, "bad projection arguments");
+  // small n_p (coarse levels, tests): fewer CTAs so none is empty
+  int nb = (n_p + kProjThreads - 1) / kProjThreads;
+  if (nb > IVK_PROJECT_BLOCKS) nb = IVK_PROJECT_BLOCKS;
+  const dim3 grid(nb, stages);
+  cudaStream_t st = as_stream(stream);
+  project_partial_kernel<<<grid, kProjThreads, 0, st>>>(n_u, n_p, x, scratch);
+  int rc = check_launch("ivk_project_pressure_means");
+  if (rc) return rc;
+  project_subtract_kernel<<<grid, kProjThreads, 0, st>>>(n_u, n_p, x, scratch);
   return check_launch("ivk_project_pressure_means");
 }
 

@@ -2717,15 +2717,13 @@ int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int3
       return check_launch("ivk_patch_factor(kron, global)");
     }
     const size_t smem = 2 * (size_t)bmax * bmax * sizeof(double);
-    static size_t configured = 0;
-    if (smem > configured) {
+    {  // set on every call: the attribute is per device
       cudaError_t e = cudaFuncSetAttribute(patch_factor_kron_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) {
         set_error("ivk_patch_factor: %s", cudaGetErrorString(e));
         return IVK_ECUDA;
       }
-      configured = smem;
     }
     FactorParams f = make_factor_params(op);
     PatchParams p = make_patch_params(pd);

@@ -45,6 +45,8 @@ class GeneralStageSystem:
         the end of the stage vector (``project_pressure_means``).
     """
 
+    _ivk_device_native = True   # takes / returns device tensors as well as numpy
+
     general = True
     convection = None
 
@@ -91,14 +93,21 @@ class GeneralStageSystem:
         return (offs[:, None] + self.constrained[None, :]).ravel()
 
     def project_pressure_means(self, x):
-        """Remove the per-stage mean of the pressure block in place; returns x."""
-        from ._device import is_device, ptr, stream
-        if is_device(x):
-            _lib.check(_lib.lib().ivk_project_pressure_means(
-                self.r, self.n_u, self.n_p, ptr(x), stream()), "project_pressure_means")
+        """Remove the per-stage mean of the pressure block in place; returns x.
+        Always libivk: a numpy ``x`` is projected on the device and written
+        back into the same array."""
+        from ._device import is_device, ptr, stream, upload
+        if not is_device(x):
+            arr = np.asarray(x)
+            if arr.dtype != np.float64 or arr.shape != (self.dim,):
+                raise ValueError(f"expected a float64 vector of length {self.dim}")
+            xd = upload(arr, np.float64)
+            self.project_pressure_means(xd)
+            arr[...] = xd.cpu().numpy()
             return x
-        p = np.asarray(x).reshape(self.r, self.n1)[:, self.n_u:]
-        p -= p.mean(axis=1, keepdims=True)
+        scratch = self.device_data()["tensors"]["proj_scratch"]
+        _lib.check(_lib.lib().ivk_project_pressure_means(
+            self.r, self.n_u, self.n_p, ptr(x), ptr(scratch), stream()), "project_pressure_means")
         return x
 
     def pressure_nullspace(self):
@@ -141,6 +150,9 @@ class GeneralStageSystem:
         t["sptr"], t["scol"], t["sml"] = (upload(sptr, np.int32), upload(scol, np.int32),
                                           upload(sml, np.float64))
         t["cmask"] = upload(self.cmask.astype(np.uint8), np.uint8)
+        import torch
+        t["proj_scratch"] = torch.zeros(_lib.PROJECT_BLOCKS * self.r, dtype=torch.float64,
+                                        device=t["cmask"].device)
         d = _lib.GeneralDesc()
         d.stages = self.r
         d.n = self.n1

@@ -223,6 +223,8 @@ class VankaPatchSet:
     stages share the convection Jacobian, A well diagonalisable), else full.
     """
 
+    _ivk_device_native = True   # takes / returns device tensors as well as numpy
+
     def __init__(self, system, mesh, omega=1.0, factor=True, mode="auto", scatter="patch",
                  vertices=None):
         if scatter not in ("patch", "owner"):
@@ -664,30 +666,69 @@ def apply_vanka(patches, system, x, b, omega=None, weights=None, workspace=None,
 
 
 def chebyshev_smooth(op_apply, precond, a, b, steps, x, rhs):
-    """Chebyshev-accelerated preconditioned Richardson (solvers.py:242-268).
-
-    Generic three-term recurrence over any array type (numpy or CUDA
-    tensors); the multigrid cycle uses a fused device version of it."""
+    """Chebyshev-accelerated preconditioned Richardson (solvers.py:242-268),
+    run on the device: every vector update is a libivk axpby; numpy ``x`` /
+    ``rhs`` are copied up and the result copied back (numpy callables are
+    wrapped at the edge, this package's own operators run natively).  The
+    multigrid cycle uses the fused K1/K3/K4 form in ``MGHierarchyOp._smooth``."""
+    from ._device import as_device_vector, to_host
     if not 0.0 < a < b:
         raise ValueError("Chebyshev interval must satisfy 0 < a < b")
     if steps <= 0:
         return x
-    theta = 0.5 * (b + a)
-    delta = 0.5 * (b - a)
+    n = int(np.asarray(rhs).shape[0]) if not _is_torch(rhs) else rhs.numel()
+    xd, host = as_device_vector(x, n)
+    bd, _ = as_device_vector(rhs, n)
+    apply_op = _device_callable(op_apply, host)
+    apply_pc = _device_callable(precond, host)
+    ax = _axpby
+    theta, delta = 0.5 * (b + a), 0.5 * (b - a)
     sigma1 = theta / delta
     rho = 1.0 / sigma1
-    x = x.clone() if hasattr(x, "clone") else x.copy()
-    r = rhs - op_apply(x)
-    z = precond(r)
-    d = z / theta
+    xk = xd.clone()
+    r = ax(1.0, bd, -1.0, apply_op(xk))              # r = rhs - A x
+    d = ax(1.0 / theta, apply_pc(r), 0.0, None)      # d = z / theta
     for _ in range(1, steps):
-        x += d
-        r = r - op_apply(d)
-        z = precond(r)
+        ax(1.0, xk, 1.0, d, out=xk)                  # x += d
+        r = ax(1.0, r, -1.0, apply_op(d))            # r -= A d
         rho_new = 1.0 / (2.0 * sigma1 - rho)
-        d = rho_new * rho * d + (2.0 * rho_new / delta) * z
+        d = ax(rho_new * rho, d, 2.0 * rho_new / delta, apply_pc(r))
         rho = rho_new
-    return x + d
+    out = ax(1.0, xk, 1.0, d)
+    return to_host(out) if host else out
+
+
+def _axpby(alpha, x, beta, y, out=None):
+    """out = alpha x + beta y on the device (libivk K9 vector op)."""
+    import torch
+    from ._device import ptr, stream
+    ref = x if x is not None else y
+    if out is None:
+        out = torch.empty_like(ref)
+    _lib.check(_lib.lib().ivk_axpby(ref.numel(), float(alpha), ptr(x), float(beta), ptr(y),
+                                    ptr(out), stream()), "axpby")
+    return out
+
+
+def _device_callable(f, host_semantics):
+    """Adapt an operator / preconditioner callable to device vectors.
+
+    This package's own objects (flagged ``_ivk_device_native``) take device
+    tensors directly.  With host (numpy) semantics any other callable is a
+    reference-style numpy function: it gets a numpy copy and its result is
+    copied back up."""
+    import torch
+    from ._device import as_device_vector, to_host
+    if f is None:
+        return lambda v: v
+    owner = getattr(f, "__self__", None)
+    if not host_semantics or getattr(owner, "_ivk_device_native", False):
+        return lambda v: torch.as_tensor(f(v), dtype=torch.float64, device=v.device)
+
+    def wrapped(v):
+        res = f(to_host(v))
+        return as_device_vector(res, v.numel())[0] if not _is_torch(res) else res
+    return wrapped
 
 
 # ------------------------------------------------------------ coarse solve
@@ -862,12 +903,21 @@ class MGHierarchyOp:
     CUDA graph (``use_graph=True``) and replayed.
     """
 
+    _ivk_device_native = True   # takes / returns device tensors as well as numpy
+
     def __init__(self, levels, coarse, use_graph=False):
         self.levels = levels
         self.coarse = coarse
         for k, lev in enumerate(levels[1:], start=1):
             if lev.prolong is None:
                 raise ValueError(f"level {k} is missing its prolongation")
+            if not hasattr(lev.prolong, "restrict_into"):
+                # a reference-style stage prolongation (scipy CSR, fine x
+                # coarse; bench.py:187-194): run it as a device transfer
+                from .interop import as_transfer, is_matrix
+                if not is_matrix(lev.prolong):
+                    raise TypeError(f"level {k}: prolong must be a transfer or a sparse matrix")
+                lev.prolong = as_transfer(lev.prolong, lev.system, levels[k - 1].system)
         self.use_graph = use_graph
         self._bufs = None
         self._graph = None
@@ -1089,127 +1139,112 @@ def _is_torch(v):
 
 
 def fgmres(op_apply, b, precond=None, x0=None, rtol=1e-8, atol=0.0, maxiter=100, restart=30):
-    """Flexible right-preconditioned GMRES (solvers.py:364-443).
+    """Flexible right-preconditioned GMRES (solvers.py:364-443), on the device.
 
-    Same algorithm as the reference (MGS Arnoldi, Givens rotations, restart,
-    true-residual check at each cycle end, monotone reported envelope).
-    When ``b`` is a CUDA tensor the Krylov basis lives on the device and the
-    MGS / norms / solution update run in libivk (fused, deterministic
-    reductions); only the (m+1) x m Hessenberg column travels to the host
-    once per iteration for the Givens update.  numpy ``b`` runs on the host.
-    """
+    Same algorithm and statistics as the reference: MGS Arnoldi, Givens
+    rotations, restart, the true residual at each cycle end, the monotone
+    envelope of the reported norms.  The Krylov basis, the Hessenberg matrix,
+    the rotations and the triangular solve all live in device memory (libivk
+    K9); the host reads back one scalar (the residual estimate) per
+    iteration to decide convergence.  A numpy ``b`` is copied up, solved on
+    the device and the solution returned as numpy (numpy callables are
+    wrapped at the edge; this package's own operator and V-cycle run
+    natively)."""
+    from ._device import as_device_vector, to_host
+    if restart < 1 or maxiter < 0:
+        raise ValueError("restart must be >= 1 and maxiter >= 0")
     if _is_torch(b):
         return _fgmres_device(op_apply, b, precond, x0, rtol, atol, maxiter, restart)
-    n = len(b)
-    x = np.zeros(n) if x0 is None else np.asarray(x0, dtype=float).copy()
-    if precond is None:
-        precond = lambda v: v
-    stats = KrylovStats()
-
-    r = b - op_apply(x)
-    norm0 = float(np.linalg.norm(r))
-    stats.residual_norms.append(norm0)
-    tol = max(rtol * norm0, atol)
-    if norm0 <= tol:
-        stats.final_residual = norm0
-        stats.relative_residual = 0.0 if norm0 == 0 else 1.0
-        stats.converged = True
-        return x, stats
-
-    while stats.iterations < maxiter:
-        m = min(restart, maxiter - stats.iterations)
-        V = np.zeros((m + 1, n))
-        Z = np.zeros((m, n))
-        H = np.zeros((m + 1, m))
-        cs = np.zeros(m)
-        sn = np.zeros(m)
-        g = np.zeros(m + 1)
-        beta = np.linalg.norm(r)
-        V[0] = r / beta
-        g[0] = beta
-        k = 0
-        for j in range(m):
-            Z[j] = precond(V[j])
-            w = np.array(op_apply(Z[j]), dtype=float)
-            for i in range(j + 1):
-                H[i, j] = w @ V[i]
-                w -= H[i, j] * V[i]
-            H[j + 1, j] = np.linalg.norm(w)
-            if H[j + 1, j] > 1e-300:
-                V[j + 1] = w / H[j + 1, j]
-            k = _givens_step(H, cs, sn, g, j)
-            stats.iterations += 1
-            est = abs(g[j + 1])
-            stats.residual_norms.append(est)
-            if est <= tol or stats.iterations >= maxiter:
-                break
-        y = np.linalg.solve(np.triu(H[:k, :k]), g[:k])
-        x = x + y @ Z[:k]
-        r = b - op_apply(x)
-        true_norm = float(np.linalg.norm(r))
-        stats.residual_norms[-1] = true_norm
-        if true_norm <= tol:
-            break
-
-    stats.final_residual = float(np.linalg.norm(b - op_apply(x)))
-    stats.relative_residual = stats.final_residual / norm0 if norm0 > 0 else 0.0
-    stats.converged = stats.final_residual <= tol
-    stats.residual_norms = list(np.minimum.accumulate(stats.residual_norms))
-    return x, stats
+    n = int(np.asarray(b).shape[0])
+    bd, _ = as_device_vector(b, n)
+    x0d = None if x0 is None else as_device_vector(x0, n)[0]
+    op_d = op_apply if getattr(getattr(op_apply, "__self__", None), "_ivk_device_native",
+                               False) else _device_callable(op_apply, True)
+    pc_d = None
+    if precond is not None:
+        pc_d = precond if getattr(getattr(precond, "__self__", None), "_ivk_device_native",
+                                  False) else _device_callable(precond, True)
+    x, stats = _fgmres_device(op_d, bd, pc_d, x0d, rtol, atol, maxiter, restart)
+    return to_host(x), stats
 
 
-def _givens_step(H, cs, sn, g, j):
-    """Apply the stored rotations to column j and form the new one
-    (solvers.py:409-421); returns j + 1."""
-    for i in range(j):
-        t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
-        H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
-        H[i, j] = t
-    denom = np.hypot(H[j, j], H[j + 1, j])
-    cs[j] = H[j, j] / denom
-    sn[j] = H[j + 1, j] / denom
-    H[j, j] = denom
-    H[j + 1, j] = 0.0
-    g[j + 1] = -sn[j] * g[j]
-    g[j] = cs[j] * g[j]
-    return j + 1
+class _KrylovWorkspace:
+    """Device storage of one FGMRES restart cycle, allocated once per
+    (n, restart) and reused (uninitialised: every row is written before it
+    is read)."""
+
+    def __init__(self, n, m, device):
+        import torch
+        f64 = dict(dtype=torch.float64, device=device)
+        self.n, self.m = n, m
+        self.V = torch.empty(m + 1, n, **f64)
+        self.Z = torch.empty(m, n, **f64)
+        self.w = torch.empty(n, **f64)
+        self.r = torch.empty(n, **f64)
+        self.tmp = torch.empty(n, **f64)
+        self.H = torch.zeros((m + 1) * m + 1, **f64)   # column-major, ld = m + 1
+        self.rot = torch.zeros(3 * (m + 1), **f64)     # cs | sn | g
+        self.y = torch.zeros(m + 1, **f64)
+        self.scal = torch.zeros(4, **f64)              # norm / est scratch
+        self.red = _lib.reduction_scratch()
+        self.host = torch.zeros(4, dtype=torch.float64).pin_memory()
 
 
 def _fgmres_device(op_apply, b, precond, x0, rtol, atol, maxiter, restart):
     import torch
     from ._device import ptr, stream
     L = _lib.lib()
-    dev_ = b.device
     n = b.numel()
-    f64 = dict(dtype=torch.float64, device=dev_)
+    f64 = dict(dtype=torch.float64, device=b.device)
     x = torch.zeros(n, **f64) if x0 is None else torch.as_tensor(x0, **f64).clone()
     if precond is None:
         precond = lambda v: v
     stats = KrylovStats()
-    scal = torch.zeros(1, **f64)
-
-    def norm(v):
-        _lib.check(L.ivk_norm(n, ptr(v), ptr(scal), stream()), "norm")
-        return float(scal.item())
-
-    def residual(xv):
-        out = torch.empty(n, **f64)
-        _lib.check(L.ivk_axpby(n, 1.0, ptr(b), -1.0, ptr(op_apply(xv)), ptr(out), stream()),
-                   "residual")
-        return out
 
     # Allocation-free fast paths for this package's own operator / cycle.
     pre_to = None
+    owner = None
     if getattr(precond, "__func__", None) is MGHierarchyOp.precondition:
-        pre_to = precond.__self__.precondition_to
+        owner = precond.__self__
+        pre_to = owner.precondition_to
     op_into = None
     if getattr(getattr(op_apply, "__self__", None), "apply_into", None) is not None and \
             getattr(op_apply, "__name__", "") == "matvec":
         sysobj = op_apply.__self__
         op_into = lambda v, out: sysobj.apply_into(v, None, out)
 
-    r = residual(x)
-    norm0 = norm(r)
+    m_max = max(1, min(restart, maxiter))
+    ws = None
+    if owner is not None:
+        ws = getattr(owner, "_krylov_ws", None)
+        if ws is not None and (ws.n != n or ws.m < m_max or ws.V.device != b.device):
+            ws = None
+    if ws is None:
+        ws = _KrylovWorkspace(n, m_max, b.device)
+        if owner is not None:
+            owner._krylov_ws = ws
+    ld = ws.m + 1
+    cs, sn, g = ws.rot[:ld], ws.rot[ld:2 * ld], ws.rot[2 * ld:]
+    st = stream()
+
+    def read(k):
+        """Device scalar ws.scal[k] -> host (one small D2H)."""
+        ws.host[k:k + 1].copy_(ws.scal[k:k + 1], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return float(ws.host[k])
+
+    def residual_norm(xv):
+        """ws.r = b - A x; returns ||ws.r||."""
+        if op_into is not None:
+            op_into(xv, ws.tmp)
+            ax = ws.tmp
+        else:
+            ax = torch.as_tensor(op_apply(xv), **f64)
+        _lib.check(L.ivk_axpby(n, 1.0, ptr(b), -1.0, ptr(ax), ptr(ws.r), st), "residual")
+        _lib.check(L.ivk_norm(n, ptr(ws.r), ptr(ws.scal), ptr(ws.red), st), "norm")
+        return read(0)
+
+    norm0 = residual_norm(x)
     stats.residual_norms.append(norm0)
     tol = max(rtol * norm0, atol)
     if norm0 <= tol:
@@ -1218,48 +1253,43 @@ def _fgmres_device(op_apply, b, precond, x0, rtol, atol, maxiter, restart):
         stats.converged = True
         return x, stats
 
-    w = torch.empty(n, **f64)
+    beta = norm0
     while stats.iterations < maxiter:
         m = min(restart, maxiter - stats.iterations)
-        V = torch.zeros(m + 1, n, **f64)
-        Z = torch.zeros(m, n, **f64)
-        hdev = torch.zeros(m + 2, **f64)
-        H = np.zeros((m + 1, m))
-        cs = np.zeros(m)
-        sn = np.zeros(m)
-        g = np.zeros(m + 1)
-        beta = norm(r)
-        _lib.check(L.ivk_axpby(n, 1.0 / beta, ptr(r), 0.0, None, ptr(V[0]), stream()), "scale")
-        g[0] = beta
+        # V_0 = r / beta, g = beta e_0 (device)
+        _lib.check(L.ivk_axpby(n, 1.0 / beta, ptr(ws.r), 0.0, None, ptr(ws.V[0]), st), "scale")
+        g.zero_()
+        g[0:1].fill_(beta)
         k = 0
         for j in range(m):
             if pre_to is not None:
-                pre_to(V[j], Z[j])
+                pre_to(ws.V[j], ws.Z[j])
             else:
-                Z[j].copy_(precond(V[j]))
+                ws.Z[j].copy_(torch.as_tensor(precond(ws.V[j]), **f64))
             if op_into is not None:
-                op_into(Z[j], w)
+                op_into(ws.Z[j], ws.w)
             else:
-                w.copy_(torch.as_tensor(op_apply(Z[j]), **f64))
-            _lib.check(L.ivk_mgs(n, ptr(V), n, j + 1, ptr(w), ptr(hdev), ptr(V[j + 1]), stream()),
-                       "mgs")
-            H[:j + 2, j] = hdev[:j + 2].cpu().numpy()
-            k = _givens_step(H, cs, sn, g, j)
+                ws.w.copy_(torch.as_tensor(op_apply(ws.Z[j]), **f64))
+            hcol = ws.H[j * ld:]
+            _lib.check(L.ivk_mgs(n, ptr(ws.V), n, j + 1, ptr(ws.w), ptr(hcol), ptr(ws.V[j + 1]),
+                                 ptr(ws.red), st), "mgs")
+            _lib.check(L.ivk_givens(j, ld, ptr(ws.H), ptr(cs), ptr(sn), ptr(g), ptr(ws.scal[1:]),
+                                    st), "givens")
+            k = j + 1
             stats.iterations += 1
-            est = abs(g[j + 1])
+            est = read(1)
             stats.residual_norms.append(est)
             if est <= tol or stats.iterations >= maxiter:
                 break
-        y = np.linalg.solve(np.triu(H[:k, :k]), g[:k])
-        ydev = torch.as_tensor(y, **f64)
-        _lib.check(L.ivk_lincomb(n, ptr(Z), n, k, ptr(ydev), ptr(x), stream()), "lincomb")
-        r = residual(x)
-        true_norm = norm(r)
+        _lib.check(L.ivk_hessenberg_solve(k, ld, ptr(ws.H), ptr(g), ptr(ws.y), st), "triu solve")
+        _lib.check(L.ivk_lincomb(n, ptr(ws.Z), n, k, ptr(ws.y), ptr(x), st), "lincomb")
+        true_norm = residual_norm(x)
         stats.residual_norms[-1] = true_norm
+        beta = true_norm
         if true_norm <= tol:
             break
 
-    stats.final_residual = norm(residual(x))
+    stats.final_residual = residual_norm(x)
     stats.relative_residual = stats.final_residual / norm0 if norm0 > 0 else 0.0
     stats.converged = stats.final_residual <= tol
     stats.residual_norms = list(np.minimum.accumulate(stats.residual_norms))

@@ -75,6 +75,8 @@ class StageSystem:
         shared Jacobian.
     """
 
+    _ivk_device_native = True   # takes / returns device tensors as well as numpy
+
     def __init__(self, blocks, tableau, dt, constrained=None, convection=None):
         if dt < 0.0:
             raise ValueError("timestep must be nonnegative")
@@ -158,17 +160,21 @@ class StageSystem:
         return (offs[:, None] + self.constrained[None, :]).ravel()
 
     def project_pressure_means(self, x):
-        """Remove the per-stage constant pressure in place; returns ``x``.
-
-        Device tensors are projected by libivk; numpy arrays on the host."""
-        from ._device import is_device, ptr, stream
-        if is_device(x):
-            self.device_data()
-            _lib.check(_lib.lib().ivk_project_pressure_means(
-                self.r, self.n_u, self.n_p, ptr(x), stream()), "project_pressure_means")
+        """Remove the per-stage constant pressure in place; returns ``x``
+        (stages.py:174-178).  Always libivk (K8): a numpy ``x`` is copied to
+        the device, projected there and written back into the same array."""
+        from ._device import is_device, ptr, stream, upload
+        if not is_device(x):
+            arr = np.asarray(x)
+            if arr.dtype != np.float64 or arr.shape != (self.dim,):
+                raise ValueError(f"expected a float64 vector of length {self.dim}")
+            xd = upload(arr, np.float64)
+            self.project_pressure_means(xd)
+            arr[...] = xd.cpu().numpy()
             return x
-        _, p = self.split(x)
-        p -= p.mean(axis=1, keepdims=True)
+        scratch = self.device_data()["tensors"]["proj_scratch"]
+        _lib.check(_lib.lib().ivk_project_pressure_means(
+            self.r, self.n_u, self.n_p, ptr(x), ptr(scratch), stream()), "project_pressure_means")
         return x
 
     def pressure_nullspace(self):
@@ -266,6 +272,8 @@ class StageSystem:
         t["bt_col"] = upload(self._brows[order], np.int32)
         t["bt_val"] = upload(self._b[order], np.float64)
         t["cmask"] = upload(self.node_constrained.astype(np.uint8), np.uint8)
+        t["proj_scratch"] = torch.zeros(_lib.PROJECT_BLOCKS * self.r, dtype=torch.float64,
+                                        device=t["cmask"].device)
         n_conv = 0
         if self._conv_vals is not None:
             t["conv"] = upload(np.stack(self._conv_vals).reshape(len(self._conv_vals), -1, 4),

@@ -90,10 +90,28 @@ def _dirk2(s):
                           [1 / 2, 1 / 2], [g, 1.0 - g])
 
 
+def _dirk3(s):
+    """Alexander's 3-stage L-stable SDIRK (tableaux.py:98-111): the diagonal
+    g is the root of g^3 - 3 g^2 + 3/2 g - 1/6 in (1/6, 1/2), taken from the
+    companion-matrix roots as the reference does (same bits)."""
+    if s != 3:
+        raise KeyError
+    cand = [z.real for z in np.roots([1.0, -3.0, 1.5, -1.0 / 6.0])
+            if abs(z.imag) < 1e-12 and 0.0 < z.real < 0.5]
+    g = float(min(cand))
+    tau = 0.5 * (1.0 + g)
+    b1 = -(6.0 * g * g - 16.0 * g + 1.0) / 4.0
+    b2 = (6.0 * g * g - 20.0 * g + 5.0) / 4.0
+    return ButcherTableau("DIRK-Alexander(3)", [[g, 0.0, 0.0], [tau - g, g, 0.0], [b1, b2, g]],
+                          [b1, b2, g], [g, tau, 1.0])
+
+
 _FAMILIES = {"gauss": _gauss, "radauiia": _radau, "lobattoiiic": _lobatto,
-             "backwardeuler": _backward_euler, "dirk-pareschirusso": _dirk2}
+             "backwardeuler": _backward_euler, "dirk-pareschirusso": _dirk2,
+             "dirk-alexander": _dirk3}
 _ALIASES = {"radau": "radauiia", "lobatto": "lobattoiiic", "be": "backwardeuler",
-            "dirk2": "dirk-pareschirusso", "pareschirusso": "dirk-pareschirusso"}
+            "dirk2": "dirk-pareschirusso", "pareschirusso": "dirk-pareschirusso",
+            "alexander": "dirk-alexander", "dirk3": "dirk-alexander"}
 
 
 def tableau_lookup(family, stages):
@@ -111,4 +129,4 @@ def tableau_lookup(family, stages):
 def registry_keys():
     return [("gauss", 1), ("gauss", 2), ("gauss", 3), ("radauiia", 1), ("radauiia", 2),
             ("radauiia", 3), ("lobattoiiic", 2), ("lobattoiiic", 3), ("backwardeuler", 1),
-            ("dirk-pareschirusso", 2)]
+            ("dirk-pareschirusso", 2), ("dirk-alexander", 3)]

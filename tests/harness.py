@@ -44,8 +44,16 @@ def setup(name):
     return disc, tab, conv, case
 
 
-def oracle_levels(disc, tab, dt, conv, levels=None):
-    """Oracle operators / patches / stage prolongations on every level."""
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def oracle_levels(disc, tab, dt, conv, levels=None, threads=1):
+    """Oracle operators / patches / stage prolongations on every level
+    (``threads``: host threads for the batched patch inversions)."""
     out = []
     ks = range(disc.num_levels) if levels is None else levels
     for k in ks:
@@ -54,19 +62,19 @@ def oracle_levels(disc, tab, dt, conv, levels=None):
         op = OracleStageOperator(blk.M, blk.K, blk.B, tab.A, dt, disc.cdofs[k], convection=cm)
         mesh = disc.hier.levels[k]
         vels, idxs = oracle_patch_indices(mesh.cells, mesh.cell_to_edges, mesh.num_vertices, op)
-        pat = OraclePatches(op, vels, idxs) if k > 0 else None
+        pat = OraclePatches(op, vels, idxs, threads=threads) if k > 0 else None
         P = disc.stage_prolong(k, tab.r).matrix if k > 0 else None
         out.append({"op": op, "patches": pat, "prolong": P, "idxs": idxs})
     return out
 
 
-def oracle_mg(levels, case, mode):
+def oracle_mg(levels, case, mode, threads=1, reverse=False):
     if mode == "cheb":
         sm = dict(pre=2, post=2, accel="chebyshev", a=case["cheby_a"], b=8.0, omega=1.0,
                   weights=None)
     else:
         sm = dict(pre=2, post=2, accel="richardson", omega=0.5, weights="pou")
-    return OracleMG(levels, sm)
+    return OracleMG(levels, sm, threads=threads, reverse=reverse)
 
 
 def rel(a, b):

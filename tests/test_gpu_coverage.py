@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 TABLEAUX = [("gauss", 1), ("gauss", 2), ("gauss", 3), ("radauiia", 1), ("radauiia", 2),
             ("radauiia", 3), ("lobattoiiic", 2), ("lobattoiiic", 3), ("backwardeuler", 1),
-            ("dirk-pareschirusso", 2)]
+            ("dirk-pareschirusso", 2), ("dirk-alexander", 3)]
 
 
 def _disc(grid="diagonal", n0=4, level=1, mu=1.0):
@@ -31,8 +31,9 @@ def test_sweep_and_vcycle_every_tableau(family, stages):
     sm = SmootherSpec()
     mg, S = disc.build_mg(tab, dt, sm)
     fine = mg.levels[-1].patches
-    if family == "dirk-pareschirusso":
-        # repeated eigenvalue: no eigen-split, the modal split needs none
+    if family.startswith("dirk-"):
+        # repeated eigenvalue (PareschiRusso(2), Alexander(3) -- a single
+        # Jordan block): no eigen-split, the modal split needs none
         assert fine.mode in ("modal", "dedup")
     lv = oracle_levels(disc, tab, dt, None)
     op, pat = lv[-1]["op"], lv[-1]["patches"]
@@ -158,7 +159,8 @@ def test_residual_in_place_matches(name):
     assert rel(r.cpu().numpy(), b.cpu().numpy() - S.matvec(x.cpu().numpy())) <= 1e-13
 
 
-@pytest.mark.parametrize("family,stages", [("dirk-pareschirusso", 2), ("lobattoiiic", 3),
+@pytest.mark.parametrize("family,stages", [("dirk-pareschirusso", 2), ("dirk-alexander", 3),
+                                           ("lobattoiiic", 3),
                                            ("backwardeuler", 1), ("gauss", 3)])
 def test_modal_any_tableau(family, stages):
     """The modal split needs no eigen-split of A: non-diagonalisable DIRK

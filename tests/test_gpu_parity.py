@@ -4,11 +4,13 @@ oracle on identical seeded inputs, and against the reference goldens.
 Gates (BASELINE.json north_star):
   * K1 operator apply: rel l2 <= 1e-13
   * one relaxation sweep (W = I and PoU, from 0 and from a random x): <= 1e-12
-  * V-cycle (mg.precondition): <= 1e-12 end to end where the coarse solve is
-    well conditioned (cfg1, ns, crossed); on the RadauIIA(3) case the F9
-    decomposed protocol: down-leg intermediates <= 1e-12, up-leg with the
-    oracle's coarse output injected <= 1e-12, coarse backward error no worse
-    than SuperLU's own (x10), end to end <= 1e-8
+  * V-cycle (mg.precondition): the F9 decomposed protocol everywhere --
+    down-leg intermediates <= 1e-12, up-leg with the oracle's coarse output
+    injected <= 1e-12, coarse backward error no worse than SuperLU's own
+    (x10) -- and end to end <= 1e-12 where the coarse solve is well
+    conditioned (cfg1, ns, crossed), else <= 10x the reference's self-floor
+    (oracle vs oracle with reversed reduction order, measured in the test;
+    ~5e-10 on the RadauIIA(3) case s3)
   * FGMRES iteration counts within +-1 of the reference's
 """
 
@@ -162,14 +164,18 @@ def test_vcycle_protocol(case, mode):
     otrace = []
     zo = omg.precondition(b.copy(), otrace)
     otr = dict(otrace)
+    # the reference's self-floor: the oracle against itself
+    # with every solve_additive's reduction order reversed
+    floor = rel(oracle_mg(case.oracle, case.case, mode, reverse=True).precondition(b.copy()), zo)
     mg.trace = {}
     try:
         z = h(mg.precondition(d(b)))
         tr = {k: h(v) for k, v in mg.trace.items()}
     finally:
         mg.trace = None
+    gate = max(1e-12, 10.0 * floor)
     # golden (reference run) agrees with the oracle
-    assert rel(zo, g["precond_" + mode]) <= (1e-12 if case.name in WELL_CONDITIONED else 1e-8)
+    assert rel(zo, g["precond_" + mode]) <= gate
     # down-leg intermediates
     for k in tr:
         if k.startswith("pre_") or k.startswith("rc_") or k == "coarse_in":
@@ -187,8 +193,11 @@ def test_vcycle_protocol(case, mode):
     finally:
         mg.coarse_override = None
     assert rel(zi, zo) <= 1e-12
-    # end to end
-    assert rel(z, zo) <= (1e-12 if case.name in WELL_CONDITIONED else 1e-8)
+    # end to end: 1e-12, or 10x the reference's own self-floor where the
+    # coarse solve amplifies rounding (s3: floor ~5e-10)
+    assert rel(z, zo) <= gate
+    if case.name in WELL_CONDITIONED:
+        assert rel(z, zo) <= 1e-12
 
 
 @pytest.mark.parametrize("mode", ["cheb", "pou"])
