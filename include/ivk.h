@@ -156,6 +156,17 @@ typedef struct ivk_modal_desc {
   int32_t ncomp;
   double dt;
   double butcher_a[IVK_MAX_STAGES * IVK_MAX_STAGES];
+  /* Layout of the patch gather list / local[] (and so of idx_off, idx,
+   * dof_pos, total_m in the patch descriptor):
+   *   0 = reference: patch entry a*(nc k+1) + nc*node + comp, pressures at
+   *       a*(nc k+1) + nc k (solvers.py:160-166) -- the CTA kernel (k > 32);
+   *   1 = fragment: entry node*(nc s) + comp*s + a, then the s pressures at
+   *       nc s k + a, each patch padded to an even length -- the warp-per-
+   *       patch tensor-core kernel (k <= 32): r lands in its shared-memory
+   *       rows and the DMMA output fragments store as 16-byte pairs without
+   *       index decode.  dof_pos addresses the same local[] entries, in the
+   *       reference's per-DoF summation order, under either layout. */
+  int32_t layout;
 } ivk_modal_desc;
 
 /* Kronecker eigen-split of the patch matrices.  With all stages sharing one

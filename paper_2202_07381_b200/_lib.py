@@ -68,6 +68,7 @@ class ModalDesc(C.Structure):
     _fields_ = [
         ("stages", C.c_int32), ("ncomp", C.c_int32), ("dt", C.c_double),
         ("butcher_a", C.c_double * (IVK_MAX_STAGES * IVK_MAX_STAGES)),
+        ("layout", C.c_int32),
     ]
 
 

@@ -1042,6 +1042,17 @@ __global__ void __launch_bounds__(128) patch_gather_blocks_kernel(FactorParams o
 // E = (I + f A)^-1 for s <= 3 (explicit adjugate: I + f A is well
 // conditioned for f = dt theta >= 0 and A with eigenvalues in the right
 // half plane -- every tableau the library builds).
+// 1 / x: hardware approximation + two Newton steps (relative error at
+// rounding level; the mode matrices I + dt theta A are far from singular).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
 template <int S>
 __device__ __forceinline__ void modal_small_inv(const double* A, double f, double* E) {
   double m[S * S];
@@ -1050,9 +1061,9 @@ __device__ __forceinline__ void modal_small_inv(const double* A, double f, doubl
 #pragma unroll
     for (int j = 0; j < S; ++j) m[i * S + j] = (i == j ? 1.0 : 0.0) + f * A[i * S + j];
   if constexpr (S == 1) {
-    E[0] = 1.0 / m[0];
+    E[0] = rcp_nr(m[0]);
   } else if constexpr (S == 2) {
-    const double id = 1.0 / (m[0] * m[3] - m[1] * m[2]);
+    const double id = rcp_nr(m[0] * m[3] - m[1] * m[2]);
     E[0] = m[3] * id;
     E[1] = -m[1] * id;
     E[2] = -m[2] * id;
@@ -1061,7 +1072,7 @@ __device__ __forceinline__ void modal_small_inv(const double* A, double f, doubl
     const double c00 = m[4] * m[8] - m[5] * m[7];
     const double c01 = m[5] * m[6] - m[3] * m[8];
     const double c02 = m[3] * m[7] - m[4] * m[6];
-    const double id = 1.0 / (m[0] * c00 + m[1] * c01 + m[2] * c02);
+    const double id = rcp_nr(m[0] * c00 + m[1] * c01 + m[2] * c02);
     E[0] = c00 * id;
     E[1] = (m[2] * m[7] - m[1] * m[8]) * id;
     E[2] = (m[1] * m[5] - m[2] * m[4]) * id;
@@ -1106,11 +1117,57 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 __host__ __device__ __forceinline__ int modal_tc_tbuf(int S, int NC, int KP) {
   return KP * ((NC * S) | 1) + 8 * ((NC * S + 7) / 8);
 }
+// per warp: two record buffers (TMA), two R buffers (cp.async gathers one
+// patch ahead; the one in use turns into the T / w / v buffer after the T
+// GEMM), two sets of 4 pressure slots
 __host__ __device__ __forceinline__ int modal_tc_seg(int S, int NC, int kmax, int KP) {
   return (2 * modal_rec(S, NC, kmax) + 2 * modal_tc_tbuf(S, NC, KP) + 2 * 4 + 3) & ~3;
 }
 
-template <int S, int NC, int KP>
+// Ampere-style asynchronous 8-byte global -> shared copy (LDGSTS): the r
+// gathers land straight in the R rows, no register staging.
+__device__ __forceinline__ void cp_async8(uint32_t dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() {
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
+// L2 evict-last policy for the patch-local results (the scatter re-reads
+// them right after), created once per thread.
+__device__ __forceinline__ uint64_t keep_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_keep_pol(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_keep_pol2(double* p, double v0, double v1, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p),
+               "d"(v0), "d"(v1), "l"(pol)
+               : "memory");
+}
+
+// Land gathered value v of fragment-layout entry j (include/ivk.h layout 1:
+// node*NA + q, then the S pressures) in the R rows (stride TS) / pressures.
+// shared address of fragment-layout entry j (include/ivk.h layout 1:
+// node*NA + q, then the S pressures) in the R rows (stride TS) / pressures
+template <int NA, int TS>
+__device__ __forceinline__ uint32_t modal_slot(uint32_t R, uint32_t Rp, int j, int nak) {
+  const int al = j / NA;   // NA is a compile-time constant: a multiply-shift
+  return j < nak ? R + 8u * (al * TS + (j - al * NA)) : Rp + 8u * (j - nak);
+}
+
+// KTX = ceil(kmax / 4) K-steps of 4 nodes run for every patch, branch-free:
+// rows of R / T past a patch's k are exact zeros, so smaller patches simply
+// multiply zeros (no divergent DMMA regions, loads pipelined across steps).
+template <int S, int NC, int KP, int KTX>
 __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
     PatchParams pd, ModalParams mp, const double* __restrict__ r, double* __restrict__ local,
     int kmax) {
@@ -1119,20 +1176,21 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
   constexpr int NA = NC * S;
   constexpr int NT = (NA + 7) / 8;   // 8-column N tiles
   constexpr int NW = 8 * NT;         // padded row width of R / T
-  constexpr int MT = KP / 8, KT = KP / 4;
+  constexpr int MT = KP / 8;
   constexpr int TS = NA | 1;                    // row stride of R and T
   static_assert(KP <= 32, "one mode per lane");
+  static_assert(4 * KTX <= KP, "K steps exceed the padded node count");
   constexpr int TBUF = KP * TS + NW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int gq = lane >> 2, gk = lane & 3;
   const int recmax = modal_rec(S, NC, kmax);
   double* buf0 = modal_sm + (long)warp * modal_tc_seg(S, NC, kmax, KP);
   double* buf1 = buf0 + recmax;
-  // R: [alpha][TS], zero rows past k.  One buffer: R is read only by the T
-  // GEMM, so the next patch's r values land in it after that.
+  // R[2]: [alpha][TS] with zero rows past k, double-buffered: patch i+1's r
+  // values are gathered (cp.async) while patch i computes
   double* rsT0 = buf1 + recmax;
-  double* rsP = rsT0 + TBUF;         // the s pressures, two buffers of 4
-  double* t = rsP + 8;               // T / w / v: [i][TS]
+  double* rsP = rsT0 + 2 * TBUF;     // the s pressures, two buffers of 4
+  const uint32_t rsT0_u = smem_u32(rsT0), rsP_u = smem_u32(rsP);
   // zero the whole segment once: the tensor-core A loads below are not
   // predicated, so they read (finite) record tails, the other buffer and
   // stale rows past k -- every such value meets an exact zero in B
@@ -1144,6 +1202,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
+  const uint64_t pol = keep_policy();
   const double dt = mp.dt;
   // each CTA walks a contiguous run of patches (neighbouring vertex stars:
   // their r gathers and local[] writes share cache lines), warps interleaved
@@ -1152,6 +1211,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
   const int pbeg = blockIdx.x * chunk;
   const int pend = min(pd.num_patches, pbeg + chunk);
   int p = pbeg + warp;
+  int rz0 = 0, rz1 = 0;   // leading rows of R[0] / R[1] a gather may have left non-zero
   if (lane == 0 && p < pend) {
     const int k0 = pd.node_off[p + 1] - pd.node_off[p];
     bulk_load(buf0, pd.inv + pd.inv_off[p], modal_rec(S, NC, k0) * 8, &bars[warp][0]);
@@ -1159,17 +1219,25 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
   if (p < pend) {
     const int off0 = pd.idx_off[p];
     const int k0 = pd.node_off[p + 1] - pd.node_off[p];
-    const int blk0 = NC * k0 + 1;
-    for (int j = lane; j < S * blk0; j += 32) {
-      const int a = (j >= blk0) + (S > 2 && j >= 2 * blk0);
-      const int e = j - a * blk0;
-      const double v = __ldg(r + pd.idx[off0 + j]);
-      if (e < NC * k0) {
-        const int al = e / NC, d = e - al * NC;
-        rsT0[al * TS + d * S + a] = v;
-      } else {
-        rsP[a] = v;
-      }
+    for (int j = lane; j < S * (NC * k0 + 1); j += 32)
+      cp_async8(modal_slot<NA, TS>(rsT0_u, rsP_u, j, NA * k0), r + __ldg(pd.idx + off0 + j));
+    rz0 = k0;
+  }
+  cp_async_commit();
+  // gather indices of the next patch (one patch ahead of its r gathers)
+  int pf_idx[4];
+  int pn_off = 0, pn_k = 0, pn_m = 0;
+  {
+    const int pn = p + stride;
+    if (pn < pend) {
+      pn_off = pd.idx_off[pn];
+      pn_k = pd.node_off[pn + 1] - pd.node_off[pn];
+      pn_m = S * (NC * pn_k + 1);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = lane + 32 * u;
+      pf_idx[u] = j < pn_m ? __ldg(pd.idx + pn_off + j) : -1;
     }
   }
   uint32_t phase = 0;
@@ -1181,27 +1249,49 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
       bulk_load(slot ? buf0 : buf1, pd.inv + pd.inv_off[pn], modal_rec(S, NC, kn) * 8,
                 &bars[warp][slot ^ 1]);
     }
+    // gather the next patch's r into the other R buffer (cp.async); clear
+    // rows an earlier, larger patch left there first (rare: sizes ascend)
+    {
+      double* RN = rsT0 + (slot ^ 1) * TBUF;
+      const uint32_t RN_u = rsT0_u + 8u * ((slot ^ 1) * TBUF);
+      const uint32_t RPN_u = rsP_u + 8u * (4 * (slot ^ 1));
+      int& rzn = slot ? rz0 : rz1;
+      if (pn_k < rzn)
+        for (int e = pn_k * TS + lane; e < rzn * TS; e += 32) RN[e] = 0.0;
+      const int nak = NA * pn_k;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (pf_idx[u] >= 0)
+          cp_async8(modal_slot<NA, TS>(RN_u, RPN_u, lane + 32 * u, nak), r + pf_idx[u]);
+      for (int j = 128 + lane; j < pn_m; j += 32)
+        cp_async8(modal_slot<NA, TS>(RN_u, RPN_u, j, nak), r + __ldg(pd.idx + pn_off + j));
+      cp_async_commit();
+      rzn = pn_k;
+    }
+    // indices of the patch after next
+    {
+      const int pnn = pn + stride;
+      pn_off = pn_k = pn_m = 0;
+      if (pnn < pend) {
+        pn_off = pd.idx_off[pnn];
+        pn_k = pd.node_off[pnn + 1] - pd.node_off[pnn];
+        pn_m = S * (NC * pn_k + 1);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = lane + 32 * u;
+        pf_idx[u] = j < pn_m ? __ldg(pd.idx + pn_off + j) : -1;
+      }
+    }
     const int off = pd.idx_off[p];
     const int k = pd.node_off[p + 1] - pd.node_off[p];
-    const int blk = NC * k + 1;
     const int ld = modal_ld(k);
-    const double* R = rsT0;
+    double* t = rsT0 + slot * TBUF;    // R, then (after the T GEMM) T / w / v
+    const double* R = t;
     const double* Rp = rsP + 4 * slot;
-    // next patch: gather indices now, r values after step 1 (m <= 128 prefetched)
-    int pf_idx[4];
-    int pn_off = 0, pn_k = 0, pn_blk = 0;
-    if (pn < pend) {
-      pn_off = pd.idx_off[pn];
-      pn_k = pd.node_off[pn + 1] - pd.node_off[pn];
-      pn_blk = NC * pn_k + 1;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = lane + 32 * u;
-      pf_idx[u] = (pn < pend && j < S * pn_blk) ? __ldg(pd.idx + pn_off + j) : -1;
-    }
     mbar_wait(&bars[warp][slot], (phase >> slot) & 1u);
     phase ^= 1u << slot;
+    cp_async_wait1();   // this patch's gathers (all but the newest group) landed
     __syncwarp();
     const double* W = slot ? buf1 : buf0;
     const double* th = W + k * ld;
@@ -1215,20 +1305,19 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
 #pragma unroll
         for (int n = 0; n < NT; ++n) d[m][n][0] = d[m][n][1] = 0.0;
 #pragma unroll
-      for (int kt = 0; kt < KT; ++kt) {
-        if (4 * kt < k) {
-          const int al = 4 * kt + gk;
-          double b[NT];
+      for (int kt = 0; kt < KTX; ++kt) {
+        const int al = 4 * kt + gk;
+        double b[NT];
 #pragma unroll
-          for (int n = 0; n < NT; ++n) b[n] = R[al * TS + 8 * n + gq];
+        for (int n = 0; n < NT; ++n) b[n] = R[al * TS + 8 * n + gq];
 #pragma unroll
-          for (int m = 0; m < MT; ++m) {
-            const double a = W[al * ld + 8 * m + gq];   // rows al >= k meet R's zero rows
+        for (int m = 0; m < MT; ++m) {
+          const double a = W[al * ld + 8 * m + gq];   // rows al >= k meet R's zero rows
 #pragma unroll
-            for (int n = 0; n < NT; ++n) dmma884(d[m][n][0], d[m][n][1], a, b[n]);
-          }
+          for (int n = 0; n < NT; ++n) dmma884(d[m][n][0], d[m][n][1], a, b[n]);
         }
       }
+      __syncwarp();   // every lane's R reads are done: T overwrites R in place
 #pragma unroll
       for (int m = 0; m < MT; ++m)
 #pragma unroll
@@ -1239,9 +1328,6 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
         }
     }
     __syncwarp();
-    double pf_val[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) pf_val[u] = pf_idx[u] >= 0 ? __ldg(r + pf_idx[u]) : 0.0;
     // lane per mode i (k <= KP <= 32: one mode per lane): w_i = E_i t_i,
     // g += c^ w; E_i, w_i and c^_i stay in registers across the reduction
     const int im = lane;
@@ -1268,12 +1354,11 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
         }
       }
     }
+    // butterfly: x + y is commutative, so every lane ends with the same bits
 #pragma unroll
-    for (int a = 0; a < S; ++a) {
+    for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) g[a] += __shfl_down_sync(0xffffffffu, g[a], o);
-      g[a] = __shfl_sync(0xffffffffu, g[a], 0);
-    }
+      for (int a = 0; a < S; ++a) g[a] += __shfl_xor_sync(0xffffffffu, g[a], o);
     double rhs[S], pv[S], Ap[S];
 #pragma unroll
     for (int a = 0; a < S; ++a) {
@@ -1315,7 +1400,8 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
       for (int q = 0; q < NA; ++q) t[im * TS + q] = 0.0;
     }
     __syncwarp();
-    // U = W V; each lane writes its two D entries of every tile
+    // U = W V; each lane stores its D fragment entries (node 8m+gq, columns
+    // 8n+2gk, +1) straight to their fragment-layout slots
     {
       double d[MT][NT][2];
 #pragma unroll
@@ -1323,81 +1409,49 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
 #pragma unroll
         for (int n = 0; n < NT; ++n) d[m][n][0] = d[m][n][1] = 0.0;
 #pragma unroll
-      for (int kt = 0; kt < KT; ++kt) {
-        if (4 * kt < k) {
-          const int i = 4 * kt + gk;
-          double b[NT];
+      for (int kt = 0; kt < KTX; ++kt) {
+        const int i = 4 * kt + gk;
+        double b[NT];
 #pragma unroll
-          for (int n = 0; n < NT; ++n) b[n] = t[i * TS + 8 * n + gq];
+        for (int n = 0; n < NT; ++n) b[n] = t[i * TS + 8 * n + gq];
 #pragma unroll
-          for (int m = 0; m < MT; ++m) {
-            const double a = W[(8 * m + gq) * ld + i];   // columns i >= k meet t's zero rows
+        for (int m = 0; m < MT; ++m) {
+          const double a = W[(8 * m + gq) * ld + i];   // columns i >= k meet t's zero rows
 #pragma unroll
-            for (int n = 0; n < NT; ++n) dmma884(d[m][n][0], d[m][n][1], a, b[n]);
-          }
+          for (int n = 0; n < NT; ++n) dmma884(d[m][n][0], d[m][n][1], a, b[n]);
         }
       }
+      double* lp = local + off;
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
         const int al = 8 * m + gq;
         if (al < k) {
 #pragma unroll
-          for (int n = 0; n < NT; ++n)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int q = 8 * n + 2 * gk + h;
-              if (q < NA) {
-                const int dd = q / S, a = q - dd * S;
-                const int pos = off + a * blk + NC * al + dd;
-                st_keep(local + (pd.slot_pos ? pd.slot_pos[pos] : pos), d[m][n][h]);
-              }
+          for (int n = 0; n < NT; ++n) {
+            const int q = 8 * n + 2 * gk;
+            if constexpr (NA % 2 == 0) {
+              // off, al*NA and q are even: a 16-byte aligned pair
+              if (q < NA) st_keep_pol2(lp + al * NA + q, d[m][n][0], d[m][n][1], pol);
+            } else {
+              if (q < NA) st_keep_pol(lp + al * NA + q, d[m][n][0], pol);
+              if (q + 1 < NA) st_keep_pol(lp + al * NA + q + 1, d[m][n][1], pol);
             }
+          }
         }
       }
     }
+    // the buffer now holds v in rows < k (zeros past k)
+    if (slot) rz1 = k; else rz0 = k;
     if (lane < S) {
-      const int pos = off + lane * blk + NC * k;
       double pl = pv[0];
 #pragma unroll
       for (int a = 1; a < S; ++a)
         if (lane == a) pl = pv[a];
-      st_keep(local + (pd.slot_pos ? pd.slot_pos[pos] : pos), pl);
-    }
-    __syncwarp();
-    // land the next patch's r values; clear the rows a previous (larger)
-    // patch left behind, so the tensor-core tiles read zeros past k
-    {
-      double* RN = rsT0;
-      double* RPN = rsP + 4 * (slot ^ 1);
-      for (int e = pn_k * TS + lane; e < KP * TS; e += 32) RN[e] = 0.0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = lane + 32 * u;
-        if (pf_idx[u] >= 0) {
-          const int a = (j >= pn_blk) + (S > 2 && j >= 2 * pn_blk);
-          const int e = j - a * pn_blk;
-          if (e < NC * pn_k) {
-            const int al = e / NC, dd = e - al * NC;
-            RN[al * TS + dd * S + a] = pf_val[u];
-          } else {
-            RPN[a] = pf_val[u];
-          }
-        }
-      }
-      for (int j = 128 + lane; pn < pend && j < S * pn_blk; j += 32) {
-        const int a = (j >= pn_blk) + (S > 2 && j >= 2 * pn_blk);
-        const int e = j - a * pn_blk;
-        const double v = __ldg(r + pd.idx[pn_off + j]);
-        if (e < NC * pn_k) {
-          const int al = e / NC, dd = e - al * NC;
-          RN[al * TS + dd * S + a] = v;
-        } else {
-          RPN[a] = v;
-        }
-      }
+      st_keep_pol(local + off + NA * k + lane, pl, pol);
     }
     __syncwarp();
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // K3m for large patches (3-D: k = 65 nodes, W_s 34 KB): one CTA of
@@ -2479,16 +2533,23 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
     void (*fn)(PatchParams, ModalParams, const double*, double*, int) = nullptr;
     size_t seg_tc = 0;
     if (kmax <= 32) {
+      IVK_REQUIRE(md->layout == 1, "modal patches with k <= 32 need the fragment layout");
       // FP64 tensor-core variant (K padded to 24 or 32 node slots)
       const int KP = kmax <= 24 ? 24 : 32;
       seg_tc = (size_t)modal_tc_seg(mp.S, mp.NC, kmax, KP) * sizeof(double);
-#define IVK_TC(SS, CC)                                                                       \
-  if (mp.S == SS && mp.NC == CC)                                                             \
-    fn = KP == 24 ? patch_apply_modal_tc_kernel<SS, CC, 24> : patch_apply_modal_tc_kernel<SS, CC, 32>;
+      // K steps: ceil(kmax / 4); below 24 nodes the 24-slot kernel runs 6
+      const int ktx = KP == 24 ? ((kmax + 3) / 4 <= 5 ? 5 : 6) : ((kmax + 3) / 4 <= 7 ? 7 : 8);
+#define IVK_TC(SS, CC)                                                                         \
+  if (mp.S == SS && mp.NC == CC)                                                               \
+    fn = KP == 24 ? (ktx == 5 ? patch_apply_modal_tc_kernel<SS, CC, 24, 5>                     \
+                              : patch_apply_modal_tc_kernel<SS, CC, 24, 6>)                    \
+                  : (ktx == 7 ? patch_apply_modal_tc_kernel<SS, CC, 32, 7>                     \
+                              : patch_apply_modal_tc_kernel<SS, CC, 32, 8>);
       IVK_TC(1, 2) IVK_TC(2, 2) IVK_TC(3, 2) IVK_TC(1, 3) IVK_TC(2, 3) IVK_TC(3, 3)
 #undef IVK_TC
     }
     if (fn == nullptr && kmax <= 72) {
+      IVK_REQUIRE(md->layout == 0, "the modal CTA kernel needs the reference layout");
       // large (3-D: k = 65) patches: CTA per patch, its warps sharing the tiles
       const size_t smem = (size_t)modal_cta_smem(mp.S, mp.NC, kmax, 72) * sizeof(double);
       IVK_REQUIRE(smem <= 200 * 1024, "modal patch (k = %d) exceeds shared memory", kmax);

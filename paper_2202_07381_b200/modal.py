@@ -52,6 +52,36 @@ def _bitwise_classes(rows):
     return rep, inverse
 
 
+def fragment_layout(tables, ncomp):
+    """The K3m fragment layout (``ivk_modal_desc.layout`` = 1) of a patch
+    table: (offsets (P+1), gather list, dof_pos) with patch entry
+    ``node*(nc s) + comp*s + a`` / pressures ``nc s k + a`` and every patch
+    padded to an even length.  ``perm`` maps each reference position
+    (a*(nc k+1) + nc*node + comp, pressure a*(nc k+1) + nc k) to its
+    fragment position; dof_pos keeps the reference per-DoF owner order."""
+    t = tables
+    S, nc = t.stages, int(ncomp)
+    na = nc * S
+    m = t.sizes.astype(np.int64)
+    k = np.diff(t.node_off).astype(np.int64)
+    if not np.array_equal(m, S * (nc * k + 1)):
+        raise ValueError("patch sizes do not match the Taylor-Hood layout")
+    mpad = m + (m & 1)
+    offp = np.concatenate([[0], np.cumsum(mpad)])
+    pid = np.repeat(np.arange(len(m)), m)
+    e = np.arange(t.total_m, dtype=np.int64) - np.repeat(t.idx_off[:-1].astype(np.int64), m)
+    blk = nc * k[pid] + 1
+    a = e // blk
+    rem = e - a * blk
+    vel = rem < nc * k[pid]
+    al, dd = rem // nc, rem % nc
+    f = np.where(vel, al * na + dd * S + a, na * k[pid] + a)
+    perm = offp[:-1][pid] + f
+    idx_f = np.zeros(int(offp[-1]), dtype=np.int64)
+    idx_f[perm] = t.idx
+    return offp, idx_f, perm[t.dof_pos]
+
+
 class ModalSplit:
     def __init__(self, tableau, dt, ncomp):
         self.A = np.asarray(tableau.A, dtype=np.float64)
@@ -81,9 +111,10 @@ class ModalSplit:
                 np.concatenate([body, pad], axis=1)
         return body
 
-    def desc(self):
+    def desc(self, layout=0):
         d = _lib.ModalDesc()
         d.stages, d.ncomp, d.dt = self.s, self.nc, self.dt
+        d.layout = int(layout)
         for i in range(self.s):
             for j in range(self.s):
                 d.butcher_a[i * self.s + j] = self.A[i, j]

@@ -473,7 +473,25 @@ class VankaPatchSet:
             d["kron"] = self.kron.desc()          # keep the host struct alive
             desc.kron = C.pointer(d["kron"])
         if self.modal is not None:
-            d["modal"] = self.modal.desc()
+            # warp-per-patch tensor-core K3m (k <= 32 free nodes): fragment
+            # layout of the gather list / local[] (include/ivk.h layout = 1)
+            kmax = int(np.diff(t.node_off).max())
+            frag = kmax <= 32
+            if frag:
+                from .modal import fragment_layout
+                offp, idx_f, dpos_f = fragment_layout(t, self.system.nc)
+                if offp[-1] >= 2 ** 31:
+                    raise ValueError("patch index total exceeds int32")
+                d["idx_off"] = upload(offp, np.int32)
+                d["idx"] = upload(idx_f, np.int32)
+                d["dof_pos"] = upload(dpos_f, np.int32)
+                d["local"] = torch.empty(int(offp[-1]), dtype=torch.float64,
+                                         device=d["idx"].device)
+                desc.total_m = int(offp[-1])
+                for name in ("idx_off", "idx", "dof_pos"):
+                    setattr(desc, name, d[name].data_ptr())
+                desc.slot_pos = None
+            d["modal"] = self.modal.desc(layout=1 if frag else 0)
             desc.modal = C.pointer(d["modal"])
         if self.dedup is not None:
             dd = self.dedup

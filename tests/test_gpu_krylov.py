@@ -79,7 +79,9 @@ def test_device_fgmres_matches_oracle():
     assert isinstance(x_h, np.ndarray)
     assert st_d.converged and st_h.converged and conv_o
     assert st_d.iterations == st_h.iterations == its_o
-    assert np.allclose(st_d.residual_norms, norms_o, rtol=1e-8, atol=0)
+    # the histories agree to rounding: relative 1e-8 of the initial norm
+    # (the last entries are ~1e-10 of it, where rounding of the reductions shows)
+    assert np.allclose(st_d.residual_norms, norms_o, rtol=1e-8, atol=1e-12 * norms_o[0])
     assert np.linalg.norm(x_d.cpu().numpy() - x_o) <= 1e-9 * np.linalg.norm(x_o)
     assert np.linalg.norm(x_h - x_o) <= 1e-9 * np.linalg.norm(x_o)
     assert np.all(np.diff(st_d.residual_norms) <= 1e-12)

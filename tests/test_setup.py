@@ -74,6 +74,19 @@ def test_patch_indices_bit_exact(name):
         # owner map is the exact inverse of the gather list
         assert t.dof_ptr[-1] == t.total_m
         assert np.array_equal(t.idx[t.dof_pos], np.repeat(np.arange(t.dim), np.diff(t.dof_ptr)))
+        # the K3m fragment layout (modal.fragment_layout): same owner entries,
+        # same per-DoF order, even-aligned patches, node-major rows
+        from paper_2202_07381_b200.modal import fragment_layout
+        offp, idx_f, dpos_f = fragment_layout(t, 2)
+        assert np.all(offp % 2 == 0)
+        assert np.array_equal(idx_f[dpos_f], t.idx[t.dof_pos])
+        q = int(np.argmax(t.sizes))
+        kq = int(t.node_off[q + 1] - t.node_off[q])
+        seg = idx_f[offp[q]:offp[q] + t.sizes[q]]
+        ref = t.idx[t.idx_off[q]:t.idx_off[q + 1]]
+        blk = 2 * kq + 1
+        assert seg[2 * tab.r * 3 + 1 * tab.r + 0] == ref[0 * blk + 2 * 3 + 1]   # node 3, comp 1, a 0
+        assert np.array_equal(seg[2 * tab.r * kq:], ref[blk - 1::blk])          # pressures
         # group order: sizes ascending, vertices ascending within a size
         assert np.all(np.diff(t.sizes) >= 0)
         same = np.diff(t.sizes) == 0
