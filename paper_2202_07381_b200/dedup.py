@@ -38,6 +38,12 @@ class DedupTables:
 CLASS_TILE = 32               # kClassTile in ivk_patches.cu
 
 
+def _as_u8(perm):
+    if perm.size and int(perm.max()) > 255:
+        raise ValueError("patch too large for uint8 permutations")
+    return perm.astype(np.uint8)
+
+
 def build_dedup_tables(mesh, system, tables):
     """Classes of bitwise-identical canonical patch matrices for ``tables``."""
     if system.convection is not None:
@@ -50,8 +56,9 @@ def build_dedup_tables(mesh, system, tables):
     coords = p2_node_coords(mesh)
     vcoords = mesh.vertices
     kk = np.diff(t.node_off).astype(np.int64)
-    if kk.max() > 85:
-        raise ValueError("patch too large for uint8 permutations")
+    if int(t.sizes.max()) > 256:
+        # perm holds stage-major local positions 0 .. m-1 of the whole patch
+        raise ValueError("patch too large for uint8 permutations (m > 256)")
     slot_of = np.repeat(np.arange(P), kk)
     # canonical node order inside each patch: by (dy, dx) offset from the vertex
     off = coords[t.node] - vcoords[t.order[slot_of]]
@@ -114,6 +121,6 @@ def build_dedup_tables(mesh, system, tables):
         classes.append(np.full(len(s), c))
     tile_start = np.concatenate(starts + [[P]]).astype(np.int64)
     return DedupTables(n_classes=n_classes, class_of=class_of,
-                       perm=perm.astype(np.uint8), order=order, rep=rep,
+                       perm=_as_u8(perm), order=order, rep=rep,
                        rep_nodes=rep_nodes, rep_vertex=t.order[rep],
                        tile_start=tile_start, tile_class=np.concatenate(classes))

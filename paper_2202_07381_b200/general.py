@@ -121,8 +121,17 @@ class GeneralStageSystem:
     def M(self):
         return sp.csr_matrix((self.m, self.col, self.rowptr), shape=(self.n1, self.n1))
 
+    def mark_host_stale(self):
+        """The device operator was re-linearised; ``l`` is refreshed lazily."""
+        self._host_stale = True
+
+    def _sync_host(self):
+        if getattr(self, "_host_stale", False):
+            self.download_operator()
+
     @property
     def L(self):
+        self._sync_host()
         return sp.csr_matrix((self.l, self.col, self.rowptr), shape=(self.n1, self.n1))
 
     def materialize(self, limit=200_000):
@@ -180,6 +189,7 @@ class GeneralStageSystem:
     def download_operator(self):
         """Refresh the host ``l`` from the device CSR after a device
         re-linearisation (the coarse direct solve factorises on the host)."""
+        self._host_stale = False
         if self._dev is not None:
             self.l = self._dev["tensors"]["ml"][:, 1].cpu().numpy().copy()
 

@@ -402,6 +402,7 @@ class MHDDiscretization:
             self.assembler(start + lv, lev.system).assemble_into_system(lev.system, u0, B0)
             if lv > 0:
                 lev.patches.factor()
+                lev.system.mark_host_stale()
         s0 = mg.levels[0].system
         s0.download_operator()
         mg.coarse = coarse_direct_solve(s0)

@@ -156,6 +156,7 @@ class NSStageNewton:
                 asm.assemble_stage(lev.system, i, us[i, :n].contiguous())
             if lv > 0:
                 lev.patches.factor()
+                lev.system.mark_host_stale()
         s0 = self.mg.levels[0].system
         s0.download_convection()
         self.mg.coarse = CoarseSolver(s0, getattr(self.mg.coarse, "method", "dense"))

@@ -1090,6 +1090,7 @@ class MGHierarchyOp:
             asm.assemble_into_system(lev.system, u[:n])
             if k > 0:
                 lev.patches.factor()
+                lev.system.mark_host_stale()
         s0 = self.levels[0].system
         s0.download_convection()
         self.coarse = CoarseSolver(s0, getattr(self.coarse, "method", "dense"))

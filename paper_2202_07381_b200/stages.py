@@ -210,10 +210,20 @@ class StageSystem:
     def BT(self):
         return self.B.T.tocsr()
 
+    def mark_host_stale(self):
+        """The device convection was re-assembled (``relinearize``); the host
+        copy is refreshed lazily, on the next host-side use."""
+        self._host_stale = True
+
+    def _sync_host(self):
+        if getattr(self, "_host_stale", False):
+            self.download_convection()
+
     def convection_matrices(self):
         """Eliminated per-stage vector Jacobians (reference ``self.convection``)."""
         if self.convection is None:
             return None
+        self._sync_host()
         mats = []
         for v in self._conv_vals:
             J = ConvectionBlocks(self.n_nodes, self.blocks.rowptr, self.blocks.col, v)
@@ -348,6 +358,7 @@ class StageSystem:
     def download_convection(self):
         """Refresh the host copy of the device convection (one shared Jacobian
         or one per stage)."""
+        self._host_stale = False
         if self._dev is None or "conv" not in self._dev["tensors"]:
             return
         conv = self._dev["tensors"]["conv"]
