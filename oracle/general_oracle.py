@@ -126,10 +126,15 @@ class OracleGeneralPatches:
             mats = np.stack([A[ix][:, ix].toarray() for ix in idx])
             self.groups.append((idx, np.linalg.inv(mats)))
 
-    def solve_additive(self, resid):
+    def solve_additive(self, resid, threads=1, reverse=False):
+        """``threads`` is accepted for interface parity with ``OraclePatches``
+        (the general oracle runs single-threaded); ``reverse`` runs groups and
+        patches in the opposite order (the F9 self-floor probe)."""
         z = np.zeros_like(resid)
         n = len(resid)
-        for idx, inv in self.groups:
+        for idx, inv in (self.groups[::-1] if reverse else self.groups):
+            if reverse:
+                idx, inv = idx[::-1], inv[::-1]
             local = np.einsum("pij,pj->pi", inv, resid[idx])
             z += np.bincount(idx.ravel(), weights=local.ravel(), minlength=n)
         return z

@@ -172,3 +172,21 @@ def test_device_assembly_contribution_map():
     assert np.array_equal(rowptr, S.rowptr) and np.array_equal(col, S.col)
     assert np.max(np.abs(got - l)) <= 1e-14 * np.max(np.abs(l))
     assert len(asm.sell_pos) == len(col)
+
+
+def test_general_oracle_runs_through_shared_drivers():
+    """The general (MHD) oracle patches plug into the shared oracle drivers
+    (oracle_apply_vanka, OracleMG incl. the reversed self-floor probe) with
+    the same keyword interface as the Stokes oracle."""
+    from harness import oracle_mg
+    from oracle.irk_vanka_oracle import oracle_apply_vanka, random_rhs
+    disc, tab, case = mhd_setup("mhd16")
+    lv = mhd_oracle_levels(disc, tab, case["dt"])
+    op, pat = lv[-1]["op"], lv[-1]["patches"]
+    b = random_rhs(op, case["seed"])
+    y1 = oracle_apply_vanka(pat, op, np.zeros(op.dim), b, 0.5, threads=4)
+    y2 = oracle_apply_vanka(pat, op, np.zeros(op.dim), b, 0.5)
+    assert np.array_equal(y1, y2)
+    z = oracle_mg(lv, dict(cheby_a=2.0), "pou").precondition(b.copy())
+    zr = oracle_mg(lv, dict(cheby_a=2.0), "pou", reverse=True).precondition(b.copy())
+    assert np.linalg.norm(z - zr) <= 1e-10 * np.linalg.norm(z)
