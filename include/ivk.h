@@ -45,6 +45,37 @@ extern "C" {
  * M, K, J are stored on the scalar P2 pattern already eliminated (zero in
  * constrained rows/columns, stages.py:77-85); B rows are per scalar node with
  * (B_x, B_y) pairs, B^T rows per P1 node -- both eliminated. */
+/* Tile plan of the K1 apply (k1tiles.py; 2-D Stokes operators, n_conv == 0).
+ * Rows are grouped into geometrically compact tiles (one CTA each).  A tile
+ * stages, for all s stages, the velocity values of the scalar nodes in its
+ * ulist and the pressures of the P1 nodes in its plist in shared memory, then
+ * runs its row slices (32 rows, one warp each) against its entry stream.
+ * tile_rec[8t .. 8t+7] = (blob offset, blob words, entry offset, entries,
+ * nu, np, ns, 0).  The tile's blob (int32 words, one TMA bulk copy) is
+ *   header (nu, np, ns, entries, 0, 0, 0, 0) | ulist (nu) | plist (np) |
+ *   pad to 4 words | slices (ns x 4) | rows (ns x 32)
+ * with slice = (entry offset within the tile, wa, wb, kind): kind 0 =
+ * velocity rows (one thread per scalar node: wa scalar-P2 entries with (m, k)
+ * values, then wb B entries with (B_x, B_y)); kind 1 = pressure rows (wa B^T
+ * entries).  Entry e of lane l sits at offset + 32 e + l in ecol (16-bit
+ * column, local to the staged lists) and eval; a row id is the scalar node /
+ * P1 node, -1 for a padding lane, -(node + 2) for a constrained (identity)
+ * velocity row.  Every row keeps its CSR entry order, so the sums are the
+ * SELL kernel's bit for bit.  All arrays are device pointers; the struct
+ * itself lives on the host. */
+typedef struct ivk_k1_tiles {
+  int32_t n_tiles;
+  int32_t max_u;           /* longest staged velocity-node list           */
+  int32_t max_p;           /* longest staged P1-node list                 */
+  int32_t max_ent;         /* most entries (with padding) of one tile     */
+  int32_t max_slices;      /* most slices of one tile                     */
+  int32_t max_blob;        /* longest blob (words)                        */
+  const int32_t* tile_rec; /* n_tiles * 8                                 */
+  const int32_t* blob;
+  const uint16_t* ecol;
+  const double* eval;      /* 2 per entry                                 */
+} ivk_k1_tiles;
+
 typedef struct ivk_operator_desc {
   int32_t stages;          /* s, 1..IVK_MAX_STAGES                        */
   int32_t n_nodes;         /* scalar P2 nodes; n_u = 2 * n_nodes          */
@@ -84,6 +115,8 @@ typedef struct ivk_operator_desc {
    * B_z) triples, velocity rows in SELL-32 with one thread per node; no
    * convection). */
   int32_t ncomp;
+  /* Optional tile plan of the K1 apply (HOST pointer, or NULL: SELL kernel). */
+  const struct ivk_k1_tiles* k1_tiles;
 } ivk_operator_desc;
 
 /* Vanka vertex-star patch set (solvers.py:116-222).  Patches are laid out

@@ -32,6 +32,15 @@ class SingularPatch(IvkError):
     pass
 
 
+class K1Tiles(C.Structure):
+    _fields_ = [
+        ("n_tiles", C.c_int32), ("max_u", C.c_int32), ("max_p", C.c_int32),
+        ("max_ent", C.c_int32), ("max_slices", C.c_int32), ("max_blob", C.c_int32),
+        ("tile_rec", C.c_void_p), ("blob", C.c_void_p), ("ecol", C.c_void_p),
+        ("eval", C.c_void_p),
+    ]
+
+
 class OperatorDesc(C.Structure):
     _fields_ = [
         ("stages", C.c_int32), ("n_nodes", C.c_int32), ("n_p", C.c_int32),
@@ -47,6 +56,7 @@ class OperatorDesc(C.Structure):
         ("b_sptr", C.c_void_p), ("b_scol", C.c_void_p), ("b_sval", C.c_void_p),
         ("bt_sptr", C.c_void_p), ("bt_scol", C.c_void_p), ("bt_sval", C.c_void_p),
         ("ncomp", C.c_int32),
+        ("k1_tiles", C.POINTER(K1Tiles)),
     ]
 
 

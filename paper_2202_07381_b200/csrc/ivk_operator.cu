@@ -247,8 +247,8 @@ __global__ void __launch_bounds__(256, (NC == 0 && !LIST && S >= 2) ? 4 : 0) sta
       } else {
         double acc = 0.0;
 #pragma unroll
-        for (int t = 0; t < S; ++t) acc += op.a[i * S + t] * ku[t];
-        y = mu[i] + op.dt * acc;
+        for (int t = 0; t < S; ++t) acc = fma(op.a[i * S + t], ku[t], acc);
+        y = fma(op.dt, acc, mu[i]);
         if constexpr (NC > 1) y += op.dt * ju[i];
       }
       out[o] = b ? b[o] - y : y;
@@ -261,6 +261,10 @@ __global__ void __launch_bounds__(256, (NC == 0 && !LIST && S >= 2) ? 4 : 0) sta
 #pragma unroll
     for (int t = 0; t < S; ++t) btu[t] = 0.0;
     const int e0 = op.bt_sptr[ws], e1 = op.bt_sptr[ws + 1];
+    int al = 0;  // stages whose velocity block starts 16-byte aligned
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0)
+#pragma unroll
+      for (int t = 0; t < S; ++t) al |= (int)(((t * sd) & 1) == 0) << t;
     constexpr int U = 4;
     for (int e = e0 + lane; e < e1; e += 32 * U) {
       int nn[U];
@@ -277,9 +281,19 @@ __global__ void __launch_bounds__(256, (NC == 0 && !LIST && S >= 2) ? 4 : 0) sta
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int t = 0; t < S; ++t)
-          // (stage offsets t * sd may be odd: no 16-byte vector loads)
-          xv[u][t] = nn[u] >= 0 ? make_double2(x[t * sd + 2 * nn[u]], x[t * sd + 2 * nn[u] + 1])
-                                : make_double2(0.0, 0.0);
+          // one 16-byte load where the stage offset t * sd is even (half the
+          // L1 lookups of two 8-byte loads), else two 8-byte loads
+          {
+            const double* px = x + t * sd + 2 * (nn[u] >= 0 ? nn[u] : 0);
+            double2 v;
+            if ((al >> t) & 1) {
+              v = *reinterpret_cast<const double2*>(px);
+            } else {
+              v.x = px[0];
+              v.y = px[1];
+            }
+            xv[u][t] = nn[u] >= 0 ? v : make_double2(0.0, 0.0);
+          }
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -293,8 +307,8 @@ __global__ void __launch_bounds__(256, (NC == 0 && !LIST && S >= 2) ? 4 : 0) sta
     for (int i = 0; i < S; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int t = 0; t < S; ++t) acc += op.a[i * S + t] * btu[t];
-      const double y = op.dt * acc;
+      for (int t = 0; t < S; ++t) acc = fma(op.a[i * S + t], btu[t], acc);
+      const double y = __dmul_rn(op.dt, acc);  // (no contraction with b - y)
       const long o = i * sd + nu + q;
       out[o] = b ? b[o] - y : y;
     }
@@ -429,8 +443,8 @@ __global__ void __launch_bounds__(256) stage_apply3_kernel(OpParams op, const do
         } else {
           double acc = 0.0;
 #pragma unroll
-          for (int t = 0; t < S; ++t) acc += op.a[i * S + t] * ku[t][d];
-          y = mu[i][d] + op.dt * acc;
+          for (int t = 0; t < S; ++t) acc = fma(op.a[i * S + t], ku[t][d], acc);
+          y = fma(op.dt, acc, mu[i][d]);
         }
         out[o] = b ? b[o] - y : y;
       }
@@ -458,12 +472,252 @@ __global__ void __launch_bounds__(256) stage_apply3_kernel(OpParams op, const do
     for (int i = 0; i < S; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int t = 0; t < S; ++t) acc += op.a[i * S + t] * btu[t];
-      const double y = op.dt * acc;
+      for (int t = 0; t < S; ++t) acc = fma(op.a[i * S + t], btu[t], acc);
+      const double y = __dmul_rn(op.dt, acc);  // (no contraction with b - y)
       const long o = i * sd + nu + q;
       out[o] = b ? b[o] - y : y;
     }
   }
+}
+
+// ---- K1 tiled (2-D Stokes, NC = 0): one CTA per tile of the plan built by
+// k1tiles.py (ivk_k1_tiles in ivk.h).  Thread 0 reads the tile's 32-byte
+// record and issues three TMA bulk copies: the metadata blob (staged-node
+// lists, slice table, row ids) and the tile's whole entry stream (values and
+// 16-bit local columns) -- so all of the tile's HBM bytes are in flight at
+// once and no thread waits on a dependent index -> value -> gather chain.
+// When the blob lands, all threads stage the velocity / pressure values the
+// tile reads (all S stages, from the L2-resident x) into shared memory and
+// prefetch their rows' b; then every gather is a shared-memory load.  One
+// thread per scalar node (both components, all stages) or per P1 node; a
+// row's entries keep their CSR order, so each sum equals the SELL kernel's
+// bit for bit.
+#ifndef IVK_K1T_U
+#define IVK_K1T_U 4
+#endif
+#ifndef IVK_K1T_MAXW
+#define IVK_K1T_MAXW 16   // warps per CTA (cap)
+#endif
+
+struct TileParams {
+  const int4* __restrict__ tile_rec;   // 2 per tile
+  const int32_t* __restrict__ blob;
+  const uint16_t* __restrict__ ecol;
+  const double2* __restrict__ eval;
+  int max_u, max_p, max_ent, max_blob;
+};
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int S>
+__global__ void __launch_bounds__(32 * IVK_K1T_MAXW)
+    stage_apply_tile_kernel(OpParams op, TileParams tp, const double* __restrict__ x,
+                            const double* b, double* out) {
+  extern __shared__ __align__(16) unsigned char k1t_smem[];
+  constexpr int U = IVK_K1T_U;
+  // shared: [entry values][xs: S x nu_t (u_x, u_y)][ps: S x np_t][entry columns][blob][mbarriers]
+  double2* vals_s = reinterpret_cast<double2*>(k1t_smem);
+  double2* xs = vals_s + tp.max_ent;
+  double* ps = reinterpret_cast<double*>(xs + S * tp.max_u);
+  uint16_t* cols_s = reinterpret_cast<uint16_t*>(ps + ((S * tp.max_p + 1) & ~1));
+  int32_t* blob = reinterpret_cast<int32_t*>(cols_s + ((tp.max_ent + 7) & ~7));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(blob + ((tp.max_blob + 3) & ~3));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    const int4 r0 = tp.tile_rec[2 * blockIdx.x];  // blob offset, blob words, entry offset, entries
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bars[0], (uint32_t)r0.y * 4u);
+    bulk_copy(blob, tp.blob + r0.x, (uint32_t)r0.y * 4u, &bars[0]);
+    mbar_expect_tx(&bars[1], (uint32_t)r0.w * 18u);
+    if (r0.w) {
+      bulk_copy(vals_s, tp.eval + r0.z, (uint32_t)r0.w * 16u, &bars[1]);
+      bulk_copy(cols_s, tp.ecol + r0.z, (uint32_t)r0.w * 2u, &bars[1]);
+    }
+  }
+  __syncthreads();  // barriers initialised
+  mbar_wait(&bars[0], 0);
+  const int nu_t = blob[0], np_t = blob[1], ns = blob[2];
+  const int32_t* ulist = blob + 8;
+  const int32_t* plist = ulist + nu_t;
+  const int4* slices = reinterpret_cast<const int4*>(blob + ((8 + nu_t + np_t + 3) & ~3));
+  const int32_t* rows = reinterpret_cast<const int32_t*>(slices + ns);
+  const int nu = 2 * op.n_nodes;
+  const long sd = nu + op.n_p;
+#pragma unroll 2
+  for (int i = threadIdx.x; i < nu_t; i += blockDim.x) {
+    const long node = ulist[i];
+    double2 v[S];
+#pragma unroll
+    for (int t = 0; t < S; ++t)  // (stage offsets may be odd: no 16-byte loads)
+      v[t] = make_double2(x[t * sd + 2 * node], x[t * sd + 2 * node + 1]);
+#pragma unroll
+    for (int t = 0; t < S; ++t) xs[t * nu_t + i] = v[t];
+  }
+  for (int i = threadIdx.x; i < np_t; i += blockDim.x) {
+    const long q = plist[i];
+#pragma unroll
+    for (int t = 0; t < S; ++t) ps[t * np_t + i] = x[t * sd + nu + q];
+  }
+  // the first slice's right-hand side, in flight during the barrier waits
+  double bb[S][2];
+  {
+    const int rid = warp < ns ? rows[warp * 32 + lane] : -1;
+    const bool vel = warp < ns && slices[warp].w == 0;
+#pragma unroll
+    for (int i = 0; i < S; ++i) bb[i][0] = bb[i][1] = 0.0;
+    if (b && rid != -1) {
+      if (vel) {
+        const long n = rid < -1 ? -(rid + 2) : rid;
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+          bb[i][0] = b[i * sd + 2 * n];
+          bb[i][1] = b[i * sd + 2 * n + 1];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < S; ++i) bb[i][0] = b[i * sd + nu + rid];
+      }
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bars[1], 0);
+  for (int s = warp; s < ns; s += nw) {
+    const int4 sl = slices[s];  // entry offset in the tile, wa, wb, kind
+    const int rid = rows[s * 32 + lane];
+    const uint16_t* ec = cols_s + sl.x + lane;
+    const double2* ev = vals_s + sl.x + lane;
+    if (s != warp && b && rid != -1) {  // (more slices than warps: load b now)
+      if (sl.w == 0) {
+        const long n = rid < -1 ? -(rid + 2) : rid;
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+          bb[i][0] = b[i * sd + 2 * n];
+          bb[i][1] = b[i * sd + 2 * n + 1];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < S; ++i) bb[i][0] = b[i * sd + nu + rid];
+      }
+    }
+    if (sl.w == 0) {
+      double mu[S][2], ku[S][2];
+#pragma unroll
+      for (int t = 0; t < S; ++t) mu[t][0] = mu[t][1] = ku[t][0] = ku[t][1] = 0.0;
+#pragma unroll U
+      for (int e = 0; e < sl.y; ++e) {
+        const int c = ec[e * 32];
+        const double2 v = ev[e * 32];
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          const double2 xv = xs[t * nu_t + c];
+          mu[t][0] = fma(v.x, xv.x, mu[t][0]);
+          mu[t][1] = fma(v.x, xv.y, mu[t][1]);
+          ku[t][0] = fma(v.y, xv.x, ku[t][0]);
+          ku[t][1] = fma(v.y, xv.y, ku[t][1]);
+        }
+      }
+      ec += sl.y * 32;
+      ev += sl.y * 32;
+#pragma unroll U
+      for (int e = 0; e < sl.z; ++e) {
+        const int c = ec[e * 32];
+        const double2 v = ev[e * 32];
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          const double pv = ps[t * np_t + c];
+          ku[t][0] = fma(v.x, pv, ku[t][0]);
+          ku[t][1] = fma(v.y, pv, ku[t][1]);
+        }
+      }
+      if (rid == -1) continue;
+      const bool fixed = rid < -1;
+      const long n = fixed ? -(rid + 2) : rid;
+#pragma unroll
+      for (int i = 0; i < S; ++i)
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          const long o = i * sd + 2 * n + d;
+          double y;
+          if (fixed) {
+            y = x[o];
+          } else {
+            double acc = 0.0;
+#pragma unroll
+            for (int t = 0; t < S; ++t) acc = fma(op.a[i * S + t], ku[t][d], acc);
+            y = fma(op.dt, acc, mu[i][d]);
+          }
+          out[o] = b ? bb[i][d] - y : y;
+        }
+    } else {
+      double btu[S];
+#pragma unroll
+      for (int t = 0; t < S; ++t) btu[t] = 0.0;
+#pragma unroll U
+      for (int e = 0; e < sl.y; ++e) {
+        const int c = ec[e * 32];
+        const double2 v = ev[e * 32];
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          const double2 xv = xs[t * nu_t + c];
+          btu[t] = fma(v.x, xv.x, btu[t]);
+          btu[t] = fma(v.y, xv.y, btu[t]);
+        }
+      }
+      if (rid < 0) continue;
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < S; ++t) acc = fma(op.a[i * S + t], btu[t], acc);
+        const double y = __dmul_rn(op.dt, acc);  // (no contraction with b - y)
+        out[i * sd + nu + rid] = b ? bb[i][0] - y : y;
+      }
+    }
+  }
+}
+
+static size_t k1t_smem_bytes(int S, const ivk_k1_tiles* tl) {
+  const size_t ent = (size_t)tl->max_ent;
+  return 16 * ent + (size_t)S * 16 * tl->max_u + 8 * (((size_t)S * tl->max_p + 1) & ~(size_t)1) +
+         2 * ((ent + 7) & ~(size_t)7) + 4 * (((size_t)tl->max_blob + 3) & ~(size_t)3) + 16;
+}
+
+template <int S>
+static int launch_stage_apply_tiles(const OpParams& q, const ivk_k1_tiles* tl, const double* x,
+                                    const double* b, double* out, cudaStream_t st) {
+  TileParams tp;
+  tp.tile_rec = reinterpret_cast<const int4*>(tl->tile_rec);
+  tp.blob = tl->blob;
+  tp.ecol = tl->ecol;
+  tp.eval = reinterpret_cast<const double2*>(tl->eval);
+  tp.max_u = tl->max_u;
+  tp.max_p = tl->max_p;
+  tp.max_ent = tl->max_ent;
+  tp.max_blob = tl->max_blob;
+  const size_t smem = k1t_smem_bytes(S, tl);
+  IVK_REQUIRE(smem <= 220 * 1024, "K1 tile plan needs %zu bytes of shared memory", smem);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(stage_apply_tile_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  int warps = tl->max_slices < IVK_K1T_MAXW ? tl->max_slices : IVK_K1T_MAXW;
+  if (warps < 1) warps = 1;
+  stage_apply_tile_kernel<S><<<tl->n_tiles, 32 * warps, smem, st>>>(q, tp, x, b, out);
+  return IVK_OK;
 }
 
 template <int S>
@@ -600,6 +854,18 @@ static int stage_apply(const ivk_operator_desc* op, const int32_t* slices, int32
   IVK_REQUIRE(out != x, "out must not alias x");
   OpParams p = make_op_params(op);
   cudaStream_t st = as_stream(stream);
+  if (op->k1_tiles && !slices && op->n_conv == 0 && op->ncomp != 3) {
+    const ivk_k1_tiles* tl = op->k1_tiles;
+    IVK_REQUIRE(tl->n_tiles > 0 && tl->tile_rec && tl->blob && tl->ecol && tl->eval,
+                "K1 tile plan has a NULL array");
+    switch (op->stages) {
+      case 1: rc = launch_stage_apply_tiles<1>(p, tl, x, b, out, st); break;
+      case 2: rc = launch_stage_apply_tiles<2>(p, tl, x, b, out, st); break;
+      case 3: rc = launch_stage_apply_tiles<3>(p, tl, x, b, out, st); break;
+    }
+    if (rc) return rc;
+    return check_launch("ivk_stage_apply (tiles)");
+  }
   switch (op->stages) {
     case 1: launch_stage_apply<1>(p, op->n_conv, op->ncomp, x, b, out, slices, n_slices, st); break;
     case 2: launch_stage_apply<2>(p, op->n_conv, op->ncomp, x, b, out, slices, n_slices, st); break;

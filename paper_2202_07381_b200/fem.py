@@ -123,6 +123,9 @@ class StokesBlocks:
     b_rowptr: np.ndarray
     b_col: np.ndarray
     b_val: np.ndarray  # (nnz_b, ncomp): (B_x, B_y) in 2-D, (B_x, B_y, B_z) in 3-D
+    # optional scalar-node coordinates (vertices, then edge midpoints): only a
+    # locality hint for the K1 tile plan (k1tiles.py), never part of the maths
+    node_xy: np.ndarray = None
 
     @property
     def ncomp(self):
@@ -255,12 +258,20 @@ class _CanonicalCells:
         self.num_edges = mesh.num_edges
 
 
+def node_coordinates(mesh):
+    """Coordinates of the scalar P2 nodes: vertices, then edge midpoints."""
+    v = np.asarray(mesh.vertices, dtype=np.float64)
+    e = np.asarray(mesh.edges)
+    return np.vstack([v, 0.5 * (v[e[:, 0]] + v[e[:, 1]])])
+
+
 def assemble_blocks(mesh, mu=1.0):
     """Scalar-form M, K (times mu) and B for one mesh level.
 
     Translation-invariant: element matrices are computed on canonically
     rotated cells and duplicates are summed in value order, so patches with
     the same local geometry get bitwise-identical matrices (patch dedup)."""
+    node_xy = node_coordinates(mesh)
     mesh = _CanonicalCells(mesh)
     nodes = p2_cell_nodes(mesh)
     n_nodes = mesh.num_vertices + mesh.num_edges
@@ -297,7 +308,8 @@ def assemble_blocks(mesh, mu=1.0):
                         m=np.ascontiguousarray(mk[:, 0]),
                         k=np.ascontiguousarray(mk[:, 1]),
                         b_rowptr=b_rowptr, b_col=b_col,
-                        b_val=np.ascontiguousarray(b_val.reshape(-1, 2)))
+                        b_val=np.ascontiguousarray(b_val.reshape(-1, 2)),
+                        node_xy=node_xy)
 
 
 def assemble_convection_jacobian(mesh, blocks, u):

@@ -9,11 +9,15 @@ owns the eliminated scalar-node data on the device and keeps the
 reference's layout helpers on the host.
 """
 
+import ctypes as C
+import os
+
 import numpy as np
 import scipy.sparse as sp
 
 from . import _lib
 from .fem import ConvectionBlocks, StokesBlocks
+from .k1tiles import build_k1_tiles
 
 __all__ = ["StageSystem", "assemble_stage_operator", "to_sell"]
 
@@ -337,7 +341,28 @@ class StageSystem:
         desc.conv_s = t["conv_s"].data_ptr() if "conv_s" in t else None
         desc.nnz_s = nnz_s
         desc.ncomp = self.nc
-        self._dev = {"tensors": t, "desc": desc,
+        tiles = None
+        tile_rows = int(os.environ.get("IVK_K1_TILES", "0"))
+        if tile_rows > 0 and self.nc == 2 and n_conv == 0:
+            # K1 tile plan (k1tiles.py): rows in Hilbert-curve tiles, x staged
+            # in shared memory; the SELL copies above stay for row-list applies
+            # (shard.py) and as the A/B reference (IVK_K1_TILES=0).
+            plan = build_k1_tiles(b.rowptr, b.col, np.column_stack([self._m, self._k]),
+                                  b.b_rowptr, b.b_col, self._b, bt_rowptr, self._brows[order],
+                                  self._b[order], self.node_constrained,
+                                  xy=getattr(b, "node_xy", None), tile_rows=tile_rows)
+            tiles = _lib.K1Tiles()
+            for k in ("n_tiles", "max_u", "max_p", "max_ent", "max_slices", "max_blob"):
+                setattr(tiles, k, int(plan[k]))
+            for k, dt_ in (("tile_rec", np.int32), ("blob", np.int32), ("ecol", np.uint16),
+                           ("eval", np.float64)):
+                t["k1t_" + k] = upload(plan[k], dt_)
+                setattr(tiles, k, t["k1t_" + k].data_ptr())
+            desc.k1_tiles = C.pointer(tiles)
+            self.k1_plan_stats = {k: int(plan[k]) for k in
+                                  ("n_tiles", "n_slices", "max_u", "max_p", "max_ent", "max_slices",
+                                   "n_entries", "tile_rows")}
+        self._dev = {"tensors": t, "desc": desc, "k1_tiles": tiles,
                      "cmask_dofs": torch.from_numpy(self._cmask).to(t["cmask"].device)}
         return self._dev
 

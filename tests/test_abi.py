@@ -39,6 +39,7 @@ def test_every_declared_symbol_is_exported_and_bound():
 
 STRUCTS = {
     "ivk_operator_desc": _lib.OperatorDesc,
+    "ivk_k1_tiles": _lib.K1Tiles,
     "ivk_patch_desc": _lib.PatchDesc,
     "ivk_kron_desc": _lib.KronDesc,
     "ivk_transfer_desc": _lib.TransferDesc,
