@@ -69,10 +69,13 @@ class ConvectionAssembler:
         self._dev = None
 
     def device_data(self, sell_pos=None):
+        """``sell_pos``: a callable returning the CSR -> SELL position map of
+        the system being written (evaluated once: it is a host pass over every
+        pattern entry, far dearer than the assembly kernel itself)."""
         if self._dev is not None:
             if sell_pos is not None and "sell_pos" not in self._dev["tensors"]:
                 from ._device import upload
-                self._dev["tensors"]["sell_pos"] = upload(sell_pos, np.int32)
+                self._dev["tensors"]["sell_pos"] = upload(sell_pos(), np.int32)
                 self._dev["desc"].sell_pos = self._dev["tensors"]["sell_pos"].data_ptr()
             return self._dev
         import torch
@@ -91,7 +94,7 @@ class ConvectionAssembler:
         t["scratch"] = torch.empty(self.n_cells * 156, dtype=torch.float64,
                                    device=t["cell_geo"].device)
         if sell_pos is not None:
-            t["sell_pos"] = upload(sell_pos, np.int32)
+            t["sell_pos"] = upload(sell_pos(), np.int32)
         d = _lib.ConvectionDesc()
         d.n_cells, d.n_nodes, d.nnz = self.n_cells, self.n_nodes, len(self.col)
         d.quad = C.pointer(self.quad)
@@ -129,7 +132,7 @@ class ConvectionAssembler:
         sdev = system.device_data()
         if system._conv_vals is None or len(system._conv_vals) != 1:
             raise ValueError("system needs one shared convection Jacobian")
-        dev = self.device_data(sell_pos=system.sell_pos())
+        dev = self.device_data(sell_pos=system.sell_pos)
         t = sdev["tensors"]
         _lib.check(_lib.lib().ivk_convection_assemble(dev["desc"], ptr(u),
                                                       ptr(dev["tensors"]["scratch"]),
@@ -145,7 +148,7 @@ class ConvectionAssembler:
             raise ValueError("system needs one convection Jacobian per stage")
         if not 0 <= stage < system.r:
             raise ValueError("stage out of range")
-        dev = self.device_data(sell_pos=system.sell_pos())
+        dev = self.device_data(sell_pos=system.sell_pos)
         t = sdev["tensors"]
         conv, conv_s = t["conv"], t["conv_s"]
         _lib.check(_lib.lib().ivk_convection_assemble(

@@ -16,6 +16,7 @@
 #include <cstdlib>
 
 #include "ivk_common.cuh"
+#include "ivk_gj.cuh"
 
 namespace ivk {
 
@@ -276,27 +277,16 @@ __device__ __forceinline__ int find_col(const int32_t* __restrict__ cols, int lo
 
 constexpr int kFactorThreads = 512;
 
-// One CTA per patch; the d x d matrix lives in dynamic shared memory
-// (row-major, leading dimension d).  Local layout (solvers.py:160-165,
-// 196-211): stage block a occupies rows a*(mv+1) .. a*(mv+1)+mv, velocity
-// DoFs 2*alpha + c for the patch's free nodes, then the vertex pressure.
-__global__ void __launch_bounds__(kFactorThreads) patch_factor_kernel(FactorParams op, PatchParams pd,
-                                                                      int32_t* singular) {
-  extern __shared__ __align__(16) double A[];
-  __shared__ int piv[512];
-  __shared__ double colk[512];
-  __shared__ int s_prow;
-  __shared__ int s_bad;
-  const int p = blockIdx.x;
+// Assemble the stage-coupled d x d patch matrix (row-major, leading dimension
+// d) into shared memory.  Local layout (solvers.py:160-165, 196-211): stage
+// block a occupies rows a*(mv+1) .. a*(mv+1)+mv, velocity DoFs 2*alpha + c
+// for the patch's free nodes, then the vertex pressure.  Ends with a barrier.
+__device__ __forceinline__ void assemble_full_patch(const FactorParams& op, double* A,
+                                                    const int* __restrict__ nodes, int nk, int v) {
   const int S = op.S;
-  const int n0 = pd.node_off[p], nk = pd.node_off[p + 1] - n0;
-  const int* nodes = pd.node + n0;
-  const int v = pd.vertex[p];
   const int mv = 2 * nk, blk = mv + 1, d = S * blk;
   const int tid = threadIdx.x;
-
   for (int e = tid; e < d * d; e += blockDim.x) A[e] = 0.0;
-  if (tid == 0) s_bad = 0;
   __syncthreads();
 
   // Velocity-velocity blocks: M delta_ab + dt a_ab (K + J_a).
@@ -337,6 +327,50 @@ __global__ void __launch_bounds__(kFactorThreads) patch_factor_kernel(FactorPara
       }
   }
   __syncthreads();
+}
+
+// K7 (d <= 16 RT, TX CT): one CTA of 16 TX threads per patch; the matrix is
+// assembled in dynamic shared memory (d x ld doubles), inverted in registers
+// (ivk_gj.cuh), which leaves Inv^T with leading dimension ld there, and copied out.
+template <int TX, int RT, int CT, int MINB>
+__global__ void __launch_bounds__(16 * TX, MINB) patch_factor_reg_kernel(FactorParams op, PatchParams pd,
+                                                                         int32_t* singular) {
+  extern __shared__ __align__(16) double A[];
+  __shared__ GjScratch<false, 16 * RT, TX * CT> gj;
+  const int p = blockIdx.x;
+  const int n0 = pd.node_off[p], nk = pd.node_off[p + 1] - n0;
+  const int v = pd.vertex[p];
+  const int d = op.S * (2 * nk + 1);
+  const int tid = threadIdx.x;
+  assemble_full_patch(op, A, pd.node + n0, nk, v);
+  const int ld = (d + 3) & ~3;
+  if (!gj_invert_registers<false, TX, RT, CT>(A, nullptr, d, ld, gj)) {
+    if (tid == 0) atomicMin(singular, v);
+    return;
+  }
+  // A now holds Inv^T with leading dimension ld: a straight 16-byte copy
+  double2* out = reinterpret_cast<double2*>(pd.inv + pd.inv_off[p]);
+  const double2* src = reinterpret_cast<const double2*>(A);
+  for (int e = tid; e < d * ld / 2; e += blockDim.x) out[e] = src[e];
+}
+
+// One CTA per patch (d > 128); the d x d matrix lives in dynamic shared memory
+// (row-major, leading dimension d) through the whole elimination.
+__global__ void __launch_bounds__(kFactorThreads) patch_factor_kernel(FactorParams op, PatchParams pd,
+                                                                      int32_t* singular) {
+  extern __shared__ __align__(16) double A[];
+  __shared__ int piv[512];
+  __shared__ double colk[512];
+  __shared__ int s_prow;
+  __shared__ int s_bad;
+  const int p = blockIdx.x;
+  const int S = op.S;
+  const int n0 = pd.node_off[p], nk = pd.node_off[p + 1] - n0;
+  const int v = pd.vertex[p];
+  const int mv = 2 * nk, blk = mv + 1, d = S * blk;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_bad = 0;
+  assemble_full_patch(op, A, pd.node + n0, nk, v);
 
   // In-place Gauss-Jordan inverse with row pivoting (first max |pivot|, as
   // LAPACK idamax); columns are unscrambled at the end.
@@ -699,12 +733,11 @@ constexpr int kKronFactorThreads = 256;
 
 // One CTA per patch; for every stored eigen-block assemble M^ + dt lam S^
 // (b x b) and invert it.  Dynamic smem: 2 * bmax^2 doubles.
-__global__ void __launch_bounds__(kKronFactorThreads) patch_factor_kron_kernel(
+template <int RT, int CT, int MINB>
+__global__ void __launch_bounds__(kKronFactorThreads, MINB) patch_factor_kron_kernel(
     FactorParams op, PatchParams pd, KronParams kp, int32_t* singular) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ int piv[256];
-  __shared__ double colre[256], colim[256];
-  __shared__ int s_prow, s_bad;
+  __shared__ GjScratch<true, 16 * RT, 16 * CT> gj;
   const int p = blockIdx.x;
   const int n0 = pd.node_off[p], nk = pd.node_off[p + 1] - n0;
   const int* nodes = pd.node + n0;
@@ -712,9 +745,8 @@ __global__ void __launch_bounds__(kKronFactorThreads) patch_factor_kron_kernel(
   const int mv = 2 * nk, b = mv + 1;
   const int tid = threadIdx.x;
   double* Are = sm;
-  double* Aim = sm + b * b;
+  double* Aim = sm + b * kron_ldr(b);
   double* out = pd.inv + pd.inv_off[p];
-  if (tid == 0) s_bad = 0;
   for (int k = 0; k < kp.nblk; ++k) {
     const bool cplx = kp.is_complex[k] != 0;
     const double fre = op.dt * kp.lam_re[k], fim = op.dt * kp.lam_im[k];
@@ -755,8 +787,10 @@ __global__ void __launch_bounds__(kKronFactorThreads) patch_factor_kron_kernel(
       Aim[mv * b + r0 + 1] = fim * bv.y;
     }
     __syncthreads();
-    const bool ok = cplx ? gauss_jordan<true>(Are, Aim, b, piv, colre, colim, &s_prow, &s_bad)
-                         : gauss_jordan<false>(Are, Aim, b, piv, colre, colim, &s_prow, &s_bad);
+    // leaves G^T in Are / Aim with the leading dimension of the stored block
+    const int ldo = kp.symmetric ? b : (cplx ? kron_ldc(b) : kron_ldr(b));
+    const bool ok = cplx ? gj_invert_registers<true, 16, RT, CT>(Are, Aim, b, ldo, gj)
+                         : gj_invert_registers<false, 16, RT, CT>(Are, Aim, b, ldo, gj);
     if (!ok) {
       if (tid == 0) atomicMin(singular, v);
       return;
@@ -790,21 +824,12 @@ __global__ void __launch_bounds__(kKronFactorThreads) patch_factor_kron_kernel(
       }
       out += kron_sym_block(cplx, b);
     } else if (cplx) {
-      const int ldc = kron_ldc(b);
-      for (int e = tid; e < b * ldc; e += blockDim.x) {
-        const int j = e / ldc, i = e - j * ldc;
-        const bool in = i < b;
-        out[2 * e] = in ? Are[i * b + j] : 0.0;
-        out[2 * e + 1] = in ? Aim[i * b + j] : 0.0;
-      }
-      out += 2 * b * ldc;
+      double2* o2 = reinterpret_cast<double2*>(out);
+      for (int e = tid; e < b * ldo; e += blockDim.x) o2[e] = make_double2(Are[e], Aim[e]);
+      out += 2 * b * ldo;
     } else {
-      const int ldr = kron_ldr(b);
-      for (int e = tid; e < b * ldr; e += blockDim.x) {
-        const int j = e / ldr, i = e - j * ldr;
-        out[e] = (i < b) ? Are[i * b + j] : 0.0;
-      }
-      out += b * ldr;
+      for (int e = tid; e < b * ldo; e += blockDim.x) out[e] = Are[e];
+      out += b * ldo;
     }
     __syncthreads();
   }
@@ -1762,13 +1787,30 @@ __device__ __forceinline__ int find_sorted(const int* a, int n, int v) {
   return -1;
 }
 
+// RT > 0: every matrix of the launch fits the 16 RT x 16 CT register tile
+// (ivk_gj.cuh); RT == 0: elimination in shared memory (gauss_jordan above).
+// RT > 0 (ivk_gj.cuh): Are / Aim end up holding the TRANSPOSED inverse with
+// leading dimension ldo (they must hold d * ldo doubles); RT == 0
+// (gauss_jordan above): the inverse itself, leading dimension d.
+template <bool CPLX, int RT, int CT, class Scratch>
+__device__ __forceinline__ bool general_invert(double* Are, double* Aim, int d, int ldo,
+                                               Scratch& gj, int* piv, double* colre,
+                                               double* colim, int* s_prow, int* s_bad) {
+  if constexpr (RT > 0) return gj_invert_registers<CPLX, 16, RT, CT>(Are, Aim, d, ldo, gj);
+  else return gauss_jordan<CPLX>(Are, Aim, d, piv, colre, colim, s_prow, s_bad);
+}
+
+template <int RT, int CT>
 __global__ void __launch_bounds__(kGenFactorThreads) general_factor_kernel(
     GenFactorParams g, PatchParams pd, KronParams kp, int use_kron, int32_t* singular) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ int piv[kGenMaxD];
-  __shared__ double colre[kGenMaxD], colim[kGenMaxD];
+  constexpr bool kReg = RT > 0;
+  constexpr int kOld = kReg ? 1 : kGenMaxD;  // the shared-memory path's scratch
+  __shared__ int piv[kOld];
+  __shared__ double colre[kOld], colim[kOld];
   __shared__ int dofs[kGenMaxD];
   __shared__ int s_prow, s_bad;
+  __shared__ GjScratch<true, kReg ? 16 * RT : 1, kReg ? 16 * CT : 1> gj;
   const int p = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
   const int off = pd.idx_off[p], m = pd.idx_off[p + 1] - off, S = g.S, b = m / S;
@@ -1778,6 +1820,7 @@ __global__ void __launch_bounds__(kGenFactorThreads) general_factor_kernel(
   if (!use_kron) {
     double* A = sm;
     const int d = m;
+    const int ld = (d + 3) & ~3;
     for (int e = tid; e < d * d; e += blockDim.x) A[e] = 0.0;
     __syncthreads();
     for (int i = warp; i < b; i += nw) {
@@ -1792,20 +1835,23 @@ __global__ void __launch_bounds__(kGenFactorThreads) general_factor_kernel(
       }
     }
     __syncthreads();
-    if (!gauss_jordan<false>(A, nullptr, d, piv, colre, colim, &s_prow, &s_bad)) {
+    if (!general_invert<false, RT, CT>(A, nullptr, d, ld, gj, piv, colre, colim, &s_prow, &s_bad)) {
       if (tid == 0) atomicMin(singular, pd.vertex[p]);
       return;
     }
-    const int ld = (d + 3) & ~3;
     double* out = pd.inv + pd.inv_off[p];
     for (int e = tid; e < d * ld; e += blockDim.x) {
-      const int j = e / ld, i = e - j * ld;
-      out[e] = (i < d) ? A[(long)i * d + j] : 0.0;
+      if constexpr (kReg) {
+        out[e] = A[e];
+      } else {
+        const int j = e / ld, i = e - j * ld;
+        out[e] = (i < d) ? A[(long)i * d + j] : 0.0;
+      }
     }
     return;
   }
   double* Are = sm;
-  double* Aim = sm + b * b;
+  double* Aim = sm + b * kron_ldr(b);
   double* out = pd.inv + pd.inv_off[p];
   for (int k = 0; k < kp.nblk; ++k) {
     const bool cplx = kp.is_complex[k] != 0;
@@ -1823,28 +1869,35 @@ __global__ void __launch_bounds__(kGenFactorThreads) general_factor_kernel(
       }
     }
     __syncthreads();
-    const bool ok = cplx ? gauss_jordan<true>(Are, Aim, b, piv, colre, colim, &s_prow, &s_bad)
-                         : gauss_jordan<false>(Are, Aim, b, piv, colre, colim, &s_prow, &s_bad);
+    const int ldo = cplx ? kron_ldc(b) : kron_ldr(b);
+    const bool ok =
+        cplx ? general_invert<true, RT, CT>(Are, Aim, b, ldo, gj, piv, colre, colim, &s_prow, &s_bad)
+             : general_invert<false, RT, CT>(Are, Aim, b, ldo, gj, piv, colre, colim, &s_prow, &s_bad);
     if (!ok) {
       if (tid == 0) atomicMin(singular, pd.vertex[p]);
       return;
     }
     if (cplx) {
-      const int ldc = kron_ldc(b);
-      for (int e = tid; e < b * ldc; e += blockDim.x) {
-        const int j = e / ldc, i = e - j * ldc;
-        const bool in = i < b;
-        out[2 * e] = in ? Are[i * b + j] : 0.0;
-        out[2 * e + 1] = in ? Aim[i * b + j] : 0.0;
+      double2* o2 = reinterpret_cast<double2*>(out);
+      for (int e = tid; e < b * ldo; e += blockDim.x) {
+        if constexpr (kReg) {
+          o2[e] = make_double2(Are[e], Aim[e]);
+        } else {
+          const int j = e / ldo, i = e - j * ldo;
+          o2[e] = i < b ? make_double2(Are[i * b + j], Aim[i * b + j]) : make_double2(0.0, 0.0);
+        }
       }
-      out += 2 * b * ldc;
+      out += 2 * b * ldo;
     } else {
-      const int ldr = kron_ldr(b);
-      for (int e = tid; e < b * ldr; e += blockDim.x) {
-        const int j = e / ldr, i = e - j * ldr;
-        out[e] = (i < b) ? Are[i * b + j] : 0.0;
+      for (int e = tid; e < b * ldo; e += blockDim.x) {
+        if constexpr (kReg) {
+          out[e] = Are[e];
+        } else {
+          const int j = e / ldo, i = e - j * ldo;
+          out[e] = (i < b) ? Are[i * b + j] : 0.0;
+        }
       }
-      out += b * ldr;
+      out += b * ldo;
     }
     __syncthreads();
   }
@@ -2777,20 +2830,26 @@ int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int3
             f, p, kp, singular_dev);
       return check_launch("ivk_patch_factor(kron, global)");
     }
-    const size_t smem = 2 * (size_t)bmax * bmax * sizeof(double);
-    {  // set on every call: the attribute is per device
-      cudaError_t e = cudaFuncSetAttribute(patch_factor_kron_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) {
-        set_error("ivk_patch_factor: %s", cudaGetErrorString(e));
-        return IVK_ECUDA;
-      }
-    }
+    const size_t smem = 2 * (size_t)bmax * kron_ldr(bmax) * sizeof(double);
     FactorParams f = make_factor_params(op);
     PatchParams p = make_patch_params(pd);
     KronParams kp = make_kron(k, S);
-    patch_factor_kron_kernel<<<pd->num_patches, kKronFactorThreads, smem, as_stream(stream)>>>(
-        f, p, kp, singular_dev);
+#define IVK_K7E_REG(RT, CT, MINB)                                                              \
+  do {                                                                                         \
+    cudaError_t e = cudaFuncSetAttribute(patch_factor_kron_kernel<RT, CT, MINB>,               \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) {                                                                    \
+      set_error("ivk_patch_factor: %s", cudaGetErrorString(e));                                \
+      return IVK_ECUDA;                                                                        \
+    }                                                                                          \
+    patch_factor_kron_kernel<RT, CT, MINB>                                                     \
+        <<<pd->num_patches, kKronFactorThreads, smem, as_stream(stream)>>>(f, p, kp,           \
+                                                                          singular_dev);      \
+  } while (0)
+    if (bmax <= 32) IVK_K7E_REG(2, 2, 4);
+    else if (bmax <= 48) IVK_K7E_REG(3, 3, 3);
+    else IVK_K7E_REG(4, 4, 2);
+#undef IVK_K7E_REG
     return check_launch("ivk_patch_factor(kron)");
   }
   const int dmax = pd->max_m;
@@ -2798,7 +2857,7 @@ int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int3
     set_error("ivk_patch_factor: patch size %d > 512 unsupported", dmax);
     return IVK_EUNSUPPORTED;
   }
-  const size_t smem = (size_t)dmax * dmax * sizeof(double);
+  const size_t smem = (size_t)dmax * ((dmax + 3) & ~3) * sizeof(double);
   if (op->ncomp == 3 || smem > 220 * 1024) {
     IVK_REQUIRE(op->n_conv == 0, "large-patch factorisation supports no convection");
     FactorParams f = make_factor_params(op);
@@ -2812,14 +2871,43 @@ int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int3
           f, p, singular_dev);
     return check_launch("ivk_patch_factor(global)");
   }
+  FactorParams f = make_factor_params(op);
+  PatchParams p = make_patch_params(pd);
+  // register-resident elimination for d <= 128 (ivk_gj.cuh); the tile shape
+  // follows the level's largest patch, smaller (boundary) patches are padded
+  if (dmax <= 128 && !getenv("IVK_K7_SMEM")) {
+#define IVK_K7_REG(...) IVK_K7_REG_(__VA_ARGS__)
+#define IVK_K7_REG_(TX, RT, CT, MINB)                                                           \
+  do {                                                                                          \
+    cudaError_t e = cudaFuncSetAttribute(patch_factor_reg_kernel<TX, RT, CT, MINB>,             \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) {                                                                     \
+      set_error("ivk_patch_factor: %s", cudaGetErrorString(e));                                 \
+      return IVK_ECUDA;                                                                         \
+    }                                                                                           \
+    patch_factor_reg_kernel<TX, RT, CT, MINB>                                                   \
+        <<<pd->num_patches, 16 * TX, smem, as_stream(stream)>>>(f, p, singular_dev);            \
+  } while (0)
+    if (dmax <= 48) IVK_K7_REG(16, 3, 3, 4);
+    else if (dmax <= 64) IVK_K7_REG(16, 4, 4, 4);
+#ifndef IVK_K7_TX  // the d <= 80 tile (2-D Taylor-Hood, s = 2): A/B knobs
+#define IVK_K7_TX 16
+#define IVK_K7_CT 5
+#define IVK_K7_MINB 3
+#endif
+    else if (dmax <= 80) IVK_K7_REG(IVK_K7_TX, 5, IVK_K7_CT, IVK_K7_MINB);
+    else if (dmax <= 96) IVK_K7_REG(16, 6, 6, 2);
+    else IVK_K7_REG(32, 8, 4, 1);
+#undef IVK_K7_REG
+#undef IVK_K7_REG_
+    return check_launch("ivk_patch_factor(registers)");
+  }
   cudaError_t e = cudaFuncSetAttribute(patch_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) {
     set_error("ivk_patch_factor: %s", cudaGetErrorString(e));
     return IVK_ECUDA;
   }
-  FactorParams f = make_factor_params(op);
-  PatchParams p = make_patch_params(pd);
   patch_factor_kernel<<<pd->num_patches, kFactorThreads, smem, as_stream(stream)>>>(f, p,
                                                                                     singular_dev);
   return check_launch("ivk_patch_factor");
@@ -2883,23 +2971,34 @@ int ivk_general_patch_factor(const ivk_general_desc* op, const ivk_patch_desc* p
     IVK_REQUIRE(SS == S, "kron blocks do not cover %d stages", S);
     kp = make_kron(k, S);
     const int bmax = pd->max_m / S;
-    smem = 2 * (size_t)bmax * bmax * sizeof(double);
+    smem = 2 * (size_t)bmax * kron_ldr(bmax) * sizeof(double);
   } else {
-    smem = (size_t)pd->max_m * pd->max_m * sizeof(double);
+    smem = (size_t)pd->max_m * ((pd->max_m + 3) & ~3) * sizeof(double);
   }
   if (smem > 200 * 1024) {
     set_error("ivk_general_patch_factor: patch (m = %d) exceeds shared memory", pd->max_m);
     return IVK_EUNSUPPORTED;
   }
-  cudaError_t e = cudaFuncSetAttribute(general_factor_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) {
-    set_error("ivk_general_patch_factor: %s", cudaGetErrorString(e));
-    return IVK_ECUDA;
-  }
   PatchParams p = make_patch_params(pd);
-  general_factor_kernel<<<pd->num_patches, kGenFactorThreads, smem, as_stream(stream)>>>(
-      g, p, kp, use_kron, singular_dev);
+  // largest matrix of the launch: an eigen-block (kron) or the whole patch
+  const int dmat = use_kron ? pd->max_m / S : pd->max_m;
+#define IVK_K7G(RT, CT)                                                                        \
+  do {                                                                                         \
+    cudaError_t e = cudaFuncSetAttribute(general_factor_kernel<RT, CT>,                        \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) {                                                                    \
+      set_error("ivk_general_patch_factor: %s", cudaGetErrorString(e));                        \
+      return IVK_ECUDA;                                                                        \
+    }                                                                                          \
+    general_factor_kernel<RT, CT>                                                              \
+        <<<pd->num_patches, kGenFactorThreads, smem, as_stream(stream)>>>(g, p, kp, use_kron,  \
+                                                                         singular_dev);       \
+  } while (0)
+  if (getenv("IVK_K7_SMEM") || dmat > 96) IVK_K7G(0, 0);
+  else if (dmat <= 48) IVK_K7G(3, 3);
+  else if (dmat <= 80) IVK_K7G(5, 5);
+  else IVK_K7G(6, 6);
+#undef IVK_K7G
   return check_launch("ivk_general_patch_factor");
 }
 
