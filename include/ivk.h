@@ -117,6 +117,13 @@ typedef struct ivk_operator_desc {
   int32_t ncomp;
   /* Optional tile plan of the K1 apply (HOST pointer, or NULL: SELL kernel). */
   const struct ivk_k1_tiles* k1_tiles;
+  /* Optional processing order of the SELL kernel's slices (device pointer,
+   * k1_order_n = all of them: velocity slices 0 .. ceil(n_nodes/16)-1, then
+   * ceil(n_nodes/16) + pressure slice): warp w of the grid runs slice
+   * k1_order[w], so the eight slices of a CTA can be chosen close together in
+   * space (L1 reuse of the gathered x).  NULL: memory order. */
+  const int32_t* k1_order;
+  int32_t k1_order_n;
 } ivk_operator_desc;
 
 /* Vanka vertex-star patch set (solvers.py:116-222).  Patches are laid out
@@ -327,6 +334,17 @@ int ivk_index_update(int64_t n, const int32_t* idx, double alpha, const double* 
  * from the eliminated operator (solvers.py:190-194).  Stokes only (n_conv = 0). */
 int ivk_patch_gather_blocks(const ivk_operator_desc* op, const ivk_patch_desc* pd, int32_t kmax,
                             double* Ms, double* Ks, double* C, void* stream);
+
+/* K7m: fill the modal store (pd->modal != NULL) from the gathered blocks, one
+ * warp per patch, k <= kmax <= 32 free nodes: Cholesky of M_s, cyclic Jacobi
+ * eigendecomposition of L^-1 K_s L^-T, W = L^-T V, c^, the s x s Schur
+ * inverse, written as the records described at ivk_modal_desc -- the device
+ * twin of scipy.linalg.eigh(K_s, M_s) + np.linalg.inv per patch, replacing
+ * np.linalg.inv of the stage-coupled matrix (solvers.py:169-184).
+ * singular_dev receives the smallest vertex id whose patch is singular (M_s
+ * not positive definite, H not finite or cond_1(H) >= 1e14), else untouched. */
+int ivk_modal_factor(const ivk_patch_desc* pd, int32_t kmax, const double* Ms, const double* Ks,
+                     const double* C, int32_t* singular_dev, void* stream);
 
 /* Sharded sweep over peer memory: the partial-sum
  * exchange + ordered reduction + x update of a strip-sharded sweep fused into

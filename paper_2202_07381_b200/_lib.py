@@ -57,6 +57,7 @@ class OperatorDesc(C.Structure):
         ("bt_sptr", C.c_void_p), ("bt_scol", C.c_void_p), ("bt_sval", C.c_void_p),
         ("ncomp", C.c_int32),
         ("k1_tiles", C.POINTER(K1Tiles)),
+        ("k1_order", C.c_void_p), ("k1_order_n", C.c_int32),
     ]
 
 
@@ -218,6 +219,7 @@ _SIGS = {
     "ivk_lincomb": ([C.c_int64, _P, C.c_int64, C.c_int32, _P, _P, _P], C.c_int),
     "ivk_patch_gather_blocks": ([C.POINTER(OperatorDesc), C.POINTER(PatchDesc), C.c_int32, _P,
                                  _P, _P, _P], C.c_int),
+    "ivk_modal_factor": ([C.POINTER(PatchDesc), C.c_int32, _P, _P, _P, _P, _P], C.c_int),
     "ivk_peer_combine_update": ([C.c_int32, _P, _P, _P, _P, C.c_double, _P, _P, _P], C.c_int),
     "ivk_mhd_assemble": ([C.POINTER(MHDDesc), _P, _P, _P, _P, _P, _P], C.c_int),
     "ivk_general_apply": ([C.POINTER(GeneralDesc), _P, _P, _P, _P], C.c_int),

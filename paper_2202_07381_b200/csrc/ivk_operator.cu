@@ -61,12 +61,12 @@ struct OpParams {
 // NC = 0 (Stokes), 1 (one J shared by all stages) or S (per-stage J_i).
 // LIST: only the warps (slices) listed in `slices` run -- the rows a shard's
 // patches read (shard.py); the other rows of `out` are left untouched.
-// The Stokes full-grid variant (S >= 2) is capped at 64 registers (4 CTAs, 32 warps
+// The Stokes variant (S >= 2) is capped at 64 registers (4 CTAs, 32 warps
 // per SM): its software-pipelined gathers need 78 otherwise, and the lost
 // occupancy costs more than the pipelining gains (57 -> 60 us uncapped, 51.6
 // capped, cfg2 fine level).
 template <int S, int NC, bool LIST>
-__global__ void __launch_bounds__(256, (NC == 0 && !LIST && S >= 2) ? 4 : 0) stage_apply_kernel(OpParams op, const double* __restrict__ x,
+__global__ void __launch_bounds__(256, (NC == 0 && S >= 2) ? 4 : 0) stage_apply_kernel(OpParams op, const double* __restrict__ x,
                                                           const double* b,
                                                           double* out,
                                                           const int32_t* __restrict__ slices,
@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(256, (NC == 0 && !LIST && S >= 2) ? 4 : 0) sta
 #ifndef IVK_K1_U
 #define IVK_K1_U 4
 #endif
-        constexpr int U = (!LIST && S >= 2) ? IVK_K1_U : 4;
-        if constexpr (!LIST && S >= 2) {
+        constexpr int U = (S >= 2) ? IVK_K1_U : 4;
+        if constexpr (S >= 2) {
         // software pipeline: the next batch's (col, m/k) loads are issued
         // before this batch's x gathers are consumed
         int cl[U];
@@ -865,6 +865,11 @@ static int stage_apply(const ivk_operator_desc* op, const int32_t* slices, int32
     }
     if (rc) return rc;
     return check_launch("ivk_stage_apply (tiles)");
+  }
+  if (!slices && op->k1_order && op->k1_order_n > 0 && op->ncomp != 3) {
+    // a locality order over ALL slices (stages.py): same kernel, same sums
+    slices = op->k1_order;
+    n_slices = op->k1_order_n;
   }
   switch (op->stages) {
     case 1: launch_stage_apply<1>(p, op->n_conv, op->ncomp, x, b, out, slices, n_slices, st); break;

@@ -1110,6 +1110,239 @@ __device__ __forceinline__ void modal_small_inv(const double* A, double f, doubl
   }
 }
 
+// K7m: the modal record of every patch with k <= 32 free nodes, one warp per
+// patch, straight from the gathered scalar blocks (ivk_patch_gather_blocks):
+//   M_s = L L^T (Cholesky),  C = L^-1 K_s L^-T,
+//   C = V Theta V^T by cyclic two-sided Jacobi rotations (stopping rule
+//   |c_pq| <= eps sqrt(c_pp c_qq): eigenvalues of the positive definite C to
+//   high relative accuracy, V orthogonal to rounding),  W = L^-T V,
+//   c^ = W^T c,  E_i = (I + dt theta_i A)^-1,  H = dt^2 A (sum_i |c^_i|^2 E_i) A,
+// and the record W | theta | c^ | H^-1 written where K3m streams it.
+// Replaces the batched Cholesky / eigh / inverse calls into cuSOLVER (setup).
+// Work arrays per warp in shared memory, row stride ks = kmax | 1 (column
+// walks -- lane j at row j -- hit distinct banks).  Every lane computes the
+// rotation angle from the same three broadcast entries, so all agree.
+// A patch is flagged singular when M_s is not positive definite, when H or
+// H^-1 is not finite, or when cond_1(H) >= 1e14.
+constexpr int kModalSetupWarps = 4;
+
+template <int S, int NC>
+__global__ void __launch_bounds__(kModalSetupWarps * 32) modal_factor_kernel(
+    PatchParams pd, ModalParams mp, int kmax, const double* __restrict__ Ms,
+    const double* __restrict__ Ks, const double* __restrict__ Cb, int32_t* singular) {
+  extern __shared__ __align__(16) double msm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * kModalSetupWarps + warp;
+  if (p >= pd.num_patches) return;
+  const int k = pd.node_off[p + 1] - pd.node_off[p];
+  const int ks = kmax | 1;
+  double* L = msm + (long)warp * 3 * kmax * ks;
+  double* C = L + kmax * ks;
+  double* V = C + kmax * ks;
+  const double* Mg = Ms + (long)p * kmax * kmax;
+  const double* Kg = Ks + (long)p * kmax * kmax;
+  for (int e = lane; e < k * k; e += 32) {
+    const int i = e / k, j = e - i * k;
+    L[i * ks + j] = Mg[i * kmax + j];
+    C[i * ks + j] = Kg[i * kmax + j];
+    V[i * ks + j] = i == j ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  bool bad = k < 1;
+  // Cholesky, right-looking; lane i owns row i
+  for (int j = 0; j < k && !bad; ++j) {
+    const double djj = L[j * ks + j];
+    if (!(djj > 0.0) || !(djj < 1.79e308)) { bad = true; break; }   // uniform: broadcast read
+    const double ljj = sqrt(djj);
+    __syncwarp();
+    if (lane == j) L[j * ks + j] = ljj;
+    if (lane > j && lane < k) L[lane * ks + j] /= ljj;
+    __syncwarp();
+    if (lane > j && lane < k) {
+      const double lij = L[lane * ks + j];
+      for (int t = j + 1; t <= lane; ++t) L[lane * ks + t] -= lij * L[t * ks + j];
+    }
+    __syncwarp();
+  }
+  if (bad) {
+    if (lane == 0) atomicMin(singular, pd.vertex[p]);
+    return;
+  }
+  // X = L^-1 K (lane c solves column c), then C = L^-1 X^T (lane r solves row r)
+  if (lane < k) {
+    for (int i = 0; i < k; ++i) {
+      double x = C[i * ks + lane];
+      for (int t = 0; t < i; ++t) x -= L[i * ks + t] * C[t * ks + lane];
+      C[i * ks + lane] = x / L[i * ks + i];
+    }
+  }
+  __syncwarp();
+  if (lane < k) {
+    for (int i = 0; i < k; ++i) {
+      double x = C[lane * ks + i];
+      for (int t = 0; t < i; ++t) x -= L[i * ks + t] * C[lane * ks + t];
+      C[lane * ks + i] = x / L[i * ks + i];
+    }
+  }
+  __syncwarp();
+  // symmetrise (pairs i < j, each handled once)
+  for (int e = lane; e < k * k; e += 32) {
+    const int i = e / k, j = e - i * k;
+    if (i < j) {
+      const double m = 0.5 * (C[i * ks + j] + C[j * ks + i]);
+      C[i * ks + j] = m;
+      C[j * ks + i] = m;
+    }
+  }
+  __syncwarp();
+  // cyclic Jacobi
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool rotated = false;
+    for (int pp = 0; pp < k - 1; ++pp)
+      for (int qq = pp + 1; qq < k; ++qq) {
+        const double apq = C[pp * ks + qq];
+        const double app = C[pp * ks + pp], aqq = C[qq * ks + qq];
+        if (!(fabs(apq) > 2.220446049250313e-16 * sqrt(fabs(app * aqq)))) continue;
+        rotated = true;
+        const double tau = (aqq - app) / (2.0 * apq);
+        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+        const double c = 1.0 / sqrt(1.0 + t * t), sn = t * c;
+        __syncwarp();   // the broadcast reads above precede the updates
+        if (lane < k) {   // columns pp, qq (lane = row), and V's
+          const double cjp = C[lane * ks + pp], cjq = C[lane * ks + qq];
+          C[lane * ks + pp] = c * cjp - sn * cjq;
+          C[lane * ks + qq] = sn * cjp + c * cjq;
+          const double vjp = V[lane * ks + pp], vjq = V[lane * ks + qq];
+          V[lane * ks + pp] = c * vjp - sn * vjq;
+          V[lane * ks + qq] = sn * vjp + c * vjq;
+        }
+        __syncwarp();
+        if (lane < k) {   // rows pp, qq (lane = column)
+          const double cpj = C[pp * ks + lane], cqj = C[qq * ks + lane];
+          C[pp * ks + lane] = c * cpj - sn * cqj;
+          C[qq * ks + lane] = sn * cpj + c * cqj;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          C[pp * ks + qq] = 0.0;
+          C[qq * ks + pp] = 0.0;
+        }
+        __syncwarp();
+      }
+    if (!rotated) break;
+  }
+  // W = L^-T V (lane c back-substitutes column c, in place)
+  if (lane < k) {
+    for (int i = k - 1; i >= 0; --i) {
+      double x = V[i * ks + lane];
+      for (int t = i + 1; t < k; ++t) x -= L[t * ks + i] * V[t * ks + lane];
+      V[i * ks + lane] = x / L[i * ks + i];
+    }
+  }
+  __syncwarp();
+  // record
+  const int ld = modal_ld(k);
+  double* rec = pd.inv + pd.inv_off[p];
+  double* th = rec + k * ld;
+  double* ch = th + k;
+  double* hi = ch + NC * k;
+  const int reclen = modal_rec(S, NC, k);
+  for (int e = lane; e < k * ld; e += 32) {
+    const int i = e / ld, j = e - i * ld;
+    rec[e] = j < k ? V[i * ks + j] : 0.0;
+  }
+  double ws[S * S];
+#pragma unroll
+  for (int a = 0; a < S * S; ++a) ws[a] = 0.0;
+  if (lane < k) {
+    const double theta = C[lane * ks + lane];
+    th[lane] = theta;
+    double c2 = 0.0;
+    const double* cg = Cb + (long)p * kmax * NC;
+#pragma unroll
+    for (int d = 0; d < NC; ++d) {
+      double acc = 0.0;
+      for (int a = 0; a < k; ++a) acc = fma(V[a * ks + lane], cg[a * NC + d], acc);
+      ch[lane * NC + d] = acc;
+      c2 = fma(acc, acc, c2);
+    }
+    double E[S * S];
+    modal_small_inv<S>(mp.a, mp.dt * theta, E);
+#pragma unroll
+    for (int a = 0; a < S * S; ++a) ws[a] = c2 * E[a];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int a = 0; a < S * S; ++a) ws[a] += __shfl_xor_sync(0xffffffffu, ws[a], o);
+  // H = dt^2 A ws A and its inverse (every lane the same bits)
+  double H[S * S], T1[S * S], Hi[S * S];
+#pragma unroll
+  for (int a = 0; a < S; ++a)
+#pragma unroll
+    for (int b = 0; b < S; ++b) {
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < S; ++c) acc = fma(mp.a[a * S + c], ws[c * S + b], acc);
+      T1[a * S + b] = acc;
+    }
+#pragma unroll
+  for (int a = 0; a < S; ++a)
+#pragma unroll
+    for (int b = 0; b < S; ++b) {
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < S; ++c) acc = fma(T1[a * S + c], mp.a[c * S + b], acc);
+      H[a * S + b] = mp.dt * mp.dt * acc;
+    }
+  if constexpr (S == 1) {
+    Hi[0] = 1.0 / H[0];
+  } else if constexpr (S == 2) {
+    const double det = H[0] * H[3] - H[1] * H[2];
+    Hi[0] = H[3] / det;
+    Hi[1] = -H[1] / det;
+    Hi[2] = -H[2] / det;
+    Hi[3] = H[0] / det;
+  } else {
+    const double c00 = H[4] * H[8] - H[5] * H[7];
+    const double c01 = H[5] * H[6] - H[3] * H[8];
+    const double c02 = H[3] * H[7] - H[4] * H[6];
+    const double det = H[0] * c00 + H[1] * c01 + H[2] * c02;
+    Hi[0] = c00 / det;
+    Hi[1] = (H[2] * H[7] - H[1] * H[8]) / det;
+    Hi[2] = (H[1] * H[5] - H[2] * H[4]) / det;
+    Hi[3] = c01 / det;
+    Hi[4] = (H[0] * H[8] - H[2] * H[6]) / det;
+    Hi[5] = (H[2] * H[3] - H[0] * H[5]) / det;
+    Hi[6] = c02 / det;
+    Hi[7] = (H[1] * H[6] - H[0] * H[7]) / det;
+    Hi[8] = (H[0] * H[4] - H[1] * H[3]) / det;
+  }
+  double nh = 0.0, ni = 0.0;   // 1-norms (max column sum)
+  bool finite = true;
+#pragma unroll
+  for (int b = 0; b < S; ++b) {
+    double sh = 0.0, si = 0.0;
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+      sh += fabs(H[a * S + b]);
+      si += fabs(Hi[a * S + b]);
+    }
+    nh = fmax(nh, sh);
+    ni = fmax(ni, si);
+    finite = finite && sh < 1.79e308 && si < 1.79e308;   // false for inf / NaN
+  }
+  if (lane < S * S) {
+    double v = Hi[0];
+#pragma unroll
+    for (int a = 1; a < S * S; ++a)
+      if (lane == a) v = Hi[a];
+    hi[lane] = v;
+  }
+  for (int e = k * ld + k + NC * k + S * S + lane; e < reclen; e += 32) rec[e] = 0.0;
+  if (lane == 0 && (!finite || !(nh * ni < 1e14))) atomicMin(singular, pd.vertex[p]);
+}
+
 template <int N>
 __device__ __forceinline__ void lds_vec(const double* p, double (&v)[N]) {
   if constexpr (N % 2 == 0) {
@@ -1135,12 +1368,39 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
-// R and T rows use an odd stride TS = NA | 1 (the lane-per-mode phase reads
-// and writes row i in lane i: conflict-free banks); the tensor-core B loads
-// read the padded columns NA..NW-1 past the row end (finite values of the
-// next row or the NW slack, multiplied into output columns that are dropped).
+// R and T row layout.  Up to 8 (component, stage) columns (IVK_K3M_SWZ, the
+// default): rows of 8 doubles with the column XOR-swizzled by
+// sw(row) = (row bit 1) << 2 | (row bit 2) << 1 | (row bit 3), which makes every
+// access pattern of the kernel conflict-free: the lane-per-mode phase (lane i
+// reads / writes row i, one column: the eight even rows of a half-warp get
+// eight distinct sw, odd rows sit in the other 64 bytes), the tensor-core B
+// loads (lanes (n, k) = (lane / 4, lane % 4) read row k0 + k, column n: rows
+// two apart differ in sw bit 2, so their four columns fall in different
+// halves of the row) and the D fragment stores (a 16-byte pair per lane).
+// Wider rows keep the earlier odd stride NA | 1 (conflict-free per-mode
+// phase, two-way conflicts on the B loads); there the B loads read the padded
+// columns NA..NW-1 past the row end (finite values of the next row or the NW
+// slack, multiplied into output columns that are dropped).
+#ifndef IVK_K3M_SWZ
+#define IVK_K3M_SWZ 1
+#endif
+__host__ __device__ __forceinline__ constexpr bool modal_tc_swz(int NA) {
+  return IVK_K3M_SWZ && NA <= 8;
+}
+__host__ __device__ __forceinline__ constexpr int modal_tc_ts(int NA) {
+  return modal_tc_swz(NA) ? 8 : (NA | 1);
+}
 __host__ __device__ __forceinline__ int modal_tc_tbuf(int S, int NC, int KP) {
-  return KP * ((NC * S) | 1) + 8 * ((NC * S + 7) / 8);
+  return KP * modal_tc_ts(NC * S) + 8 * ((NC * S + 7) / 8);
+}
+__device__ __forceinline__ int modal_sw(int row) {
+  return ((row << 1) & 4) | ((row >> 1) & 2) | ((row >> 3) & 1);
+}
+// element (row, col) of an R / T buffer
+template <int NA>
+__device__ __forceinline__ int modal_tpos(int row, int col) {
+  if constexpr (modal_tc_swz(NA)) return row * 8 + (col ^ modal_sw(row));
+  else return row * (NA | 1) + col;
 }
 // per warp: two record buffers (TMA), two R buffers (cp.async gathers one
 // patch ahead; the one in use turns into the T / w / v buffer after the T
@@ -1183,10 +1443,10 @@ __device__ __forceinline__ void st_keep_pol2(double* p, double v0, double v1, ui
 // node*NA + q, then the S pressures) in the R rows (stride TS) / pressures.
 // shared address of fragment-layout entry j (include/ivk.h layout 1:
 // node*NA + q, then the S pressures) in the R rows (stride TS) / pressures
-template <int NA, int TS>
+template <int NA>
 __device__ __forceinline__ uint32_t modal_slot(uint32_t R, uint32_t Rp, int j, int nak) {
   const int al = j / NA;   // NA is a compile-time constant: a multiply-shift
-  return j < nak ? R + 8u * (al * TS + (j - al * NA)) : Rp + 8u * (j - nak);
+  return j < nak ? R + 8u * modal_tpos<NA>(al, j - al * NA) : Rp + 8u * (j - nak);
 }
 
 // KTX = ceil(kmax / 4) K-steps of 4 nodes run for every patch, branch-free:
@@ -1202,7 +1462,8 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
   constexpr int NT = (NA + 7) / 8;   // 8-column N tiles
   constexpr int NW = 8 * NT;         // padded row width of R / T
   constexpr int MT = KP / 8;
-  constexpr int TS = NA | 1;                    // row stride of R and T
+  constexpr int TS = modal_tc_ts(NA);           // row stride of R and T
+  constexpr bool SWZ = modal_tc_swz(NA);
   static_assert(KP <= 32, "one mode per lane");
   static_assert(4 * KTX <= KP, "K steps exceed the padded node count");
   constexpr int TBUF = KP * TS + NW;
@@ -1245,7 +1506,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
     const int off0 = pd.idx_off[p];
     const int k0 = pd.node_off[p + 1] - pd.node_off[p];
     for (int j = lane; j < S * (NC * k0 + 1); j += 32)
-      cp_async8(modal_slot<NA, TS>(rsT0_u, rsP_u, j, NA * k0), r + __ldg(pd.idx + off0 + j));
+      cp_async8(modal_slot<NA>(rsT0_u, rsP_u, j, NA * k0), r + __ldg(pd.idx + off0 + j));
     rz0 = k0;
   }
   cp_async_commit();
@@ -1287,9 +1548,9 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         if (pf_idx[u] >= 0)
-          cp_async8(modal_slot<NA, TS>(RN_u, RPN_u, lane + 32 * u, nak), r + pf_idx[u]);
+          cp_async8(modal_slot<NA>(RN_u, RPN_u, lane + 32 * u, nak), r + pf_idx[u]);
       for (int j = 128 + lane; j < pn_m; j += 32)
-        cp_async8(modal_slot<NA, TS>(RN_u, RPN_u, j, nak), r + __ldg(pd.idx + pn_off + j));
+        cp_async8(modal_slot<NA>(RN_u, RPN_u, j, nak), r + __ldg(pd.idx + pn_off + j));
       cp_async_commit();
       rzn = pn_k;
     }
@@ -1334,7 +1595,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
         const int al = 4 * kt + gk;
         double b[NT];
 #pragma unroll
-        for (int n = 0; n < NT; ++n) b[n] = R[al * TS + 8 * n + gq];
+        for (int n = 0; n < NT; ++n) b[n] = R[modal_tpos<NA>(al, 8 * n + gq)];
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
           const double a = W[al * ld + 8 * m + gq];   // rows al >= k meet R's zero rows
@@ -1348,8 +1609,18 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           const int q0 = 8 * n + 2 * gk;
-          if (q0 < NA) t[(8 * m + gq) * TS + q0] = d[m][n][0];
-          if (q0 + 1 < NA) t[(8 * m + gq) * TS + q0 + 1] = d[m][n][1];
+          if constexpr (SWZ && NA % 2 == 0) {
+            // the pair (q0, q0 + 1) stays one aligned 16-byte slot, swapped
+            // where sw(row) is odd
+            const int row = 8 * m + gq, sw = modal_sw(row);
+            if (q0 < NA)
+              *reinterpret_cast<double2*>(t + row * 8 + ((q0 ^ sw) & ~1)) =
+                  (sw & 1) ? make_double2(d[m][n][1], d[m][n][0])
+                           : make_double2(d[m][n][0], d[m][n][1]);
+          } else {
+            if (q0 < NA) t[modal_tpos<NA>(8 * m + gq, q0)] = d[m][n][0];
+            if (q0 + 1 < NA) t[modal_tpos<NA>(8 * m + gq, q0 + 1)] = d[m][n][1];
+          }
         }
     }
     __syncwarp();
@@ -1364,7 +1635,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
     if (act) {
       double acc[NA];
 #pragma unroll
-      for (int q = 0; q < NA; ++q) acc[q] = t[im * TS + q];
+      for (int q = 0; q < NA; ++q) acc[q] = t[modal_tpos<NA>(im, q)];
       modal_small_inv<S>(mp.a, dt * th[im], E);
 #pragma unroll
       for (int dd = 0; dd < NC; ++dd) {
@@ -1418,11 +1689,12 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
 #pragma unroll
       for (int dd = 0; dd < NC; ++dd)
 #pragma unroll
-        for (int a = 0; a < S; ++a) t[im * TS + dd * S + a] = fma(-dt * cc[dd], e[a], wv[dd * S + a]);
+        for (int a = 0; a < S; ++a)
+          t[modal_tpos<NA>(im, dd * S + a)] = fma(-dt * cc[dd], e[a], wv[dd * S + a]);
     } else if (im < KP) {
       // rows past k: exact zeros for the U GEMM's unpredicated A columns
 #pragma unroll
-      for (int q = 0; q < NA; ++q) t[im * TS + q] = 0.0;
+      for (int q = 0; q < NA; ++q) t[modal_tpos<NA>(im, q)] = 0.0;
     }
     __syncwarp();
     // U = W V; each lane stores its D fragment entries (node 8m+gq, columns
@@ -1438,7 +1710,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
         const int i = 4 * kt + gk;
         double b[NT];
 #pragma unroll
-        for (int n = 0; n < NT; ++n) b[n] = t[i * TS + 8 * n + gq];
+        for (int n = 0; n < NT; ++n) b[n] = t[modal_tpos<NA>(i, 8 * n + gq)];
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
           const double a = W[(8 * m + gq) * ld + i];   // columns i >= k meet t's zero rows
@@ -2929,6 +3201,48 @@ int ivk_patch_gather_blocks(const ivk_operator_desc* op, const ivk_patch_desc* p
   else
     patch_gather_blocks_kernel<2><<<pd->num_patches, 128, 0, as_stream(stream)>>>(f, p, kmax, Ms, Ks, C);
   return check_launch("ivk_patch_gather_blocks");
+}
+
+int ivk_modal_factor(const ivk_patch_desc* pd, int32_t kmax, const double* Ms, const double* Ks,
+                     const double* C, int32_t* singular_dev, void* stream) {
+  int rc = validate_patches(pd);
+  if (rc) return rc;
+  IVK_REQUIRE(pd->modal && pd->vertex && pd->node_off && Ms && Ks && C && singular_dev,
+              "modal factorisation needs a modal store, vertex/node tables and the gathered blocks");
+  IVK_REQUIRE(kmax >= 1 && kmax <= 32, "modal factorisation: %d nodes per patch > 32 unsupported",
+              kmax);
+  const ivk_modal_desc* m = pd->modal;
+  IVK_REQUIRE(m->stages >= 1 && m->stages <= IVK_MAX_STAGES && (m->ncomp == 2 || m->ncomp == 3),
+              "bad modal descriptor");
+  ModalParams mp;
+  mp.S = m->stages;
+  mp.NC = m->ncomp;
+  mp.dt = m->dt;
+  for (int i = 0; i < IVK_MAX_STAGES * IVK_MAX_STAGES; ++i) mp.a[i] = m->butcher_a[i];
+  PatchParams p = make_patch_params(pd);
+  const size_t smem = (size_t)kModalSetupWarps * 3 * kmax * (kmax | 1) * sizeof(double);
+  const int grid = (pd->num_patches + kModalSetupWarps - 1) / kModalSetupWarps;
+#define IVK_K7M(SS, CC)                                                                          \
+  do {                                                                                           \
+    cudaError_t e = cudaFuncSetAttribute(modal_factor_kernel<SS, CC>,                            \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) {                                                                      \
+      set_error("ivk_modal_factor: %s", cudaGetErrorString(e));                                  \
+      return IVK_ECUDA;                                                                          \
+    }                                                                                            \
+    modal_factor_kernel<SS, CC><<<grid, kModalSetupWarps * 32, smem, as_stream(stream)>>>(       \
+        p, mp, kmax, Ms, Ks, C, singular_dev);                                                   \
+  } while (0)
+  switch (mp.S * 10 + mp.NC) {
+    case 12: IVK_K7M(1, 2); break;
+    case 22: IVK_K7M(2, 2); break;
+    case 32: IVK_K7M(3, 2); break;
+    case 13: IVK_K7M(1, 3); break;
+    case 23: IVK_K7M(2, 3); break;
+    case 33: IVK_K7M(3, 3); break;
+  }
+#undef IVK_K7M
+  return check_launch("ivk_modal_factor");
 }
 
 int ivk_peer_combine_update(int32_t n, const int32_t* dofs, const int32_t* holder_ptr,

@@ -11,10 +11,14 @@ carried by ``W_s`` (k x k), ``theta`` (k), ``c^ = (W_s (x) I)^T b`` (k nc) and
 the s x s inverse of the pressure Schur complement
 ``H = dt^2 A (sum_id c^_id^2 (I + dt theta_i A)^-1) A`` -- for the cfg2
 interior patch 446 doubles instead of 4,563 (kron) or 13,689 (full), for any
-Butcher tableau.  Setup (kernel ``ivk_patch_gather_blocks`` + batched
-Cholesky / eigh / inverses on the device) replaces ``np.linalg.inv``; the
-apply is kernel K3m (``ivk_patch_apply`` with ``pd->modal``).
+Butcher tableau.  Setup (kernels ``ivk_patch_gather_blocks`` + K7m
+``ivk_modal_factor``: Cholesky, Jacobi eigensolver and record assembly, a
+warp per patch; patches with more than 32 nodes: batched torch.linalg calls)
+replaces ``np.linalg.inv``; the apply is kernel K3m (``ivk_patch_apply`` with
+``pd->modal``).
 """
+
+import os
 
 import numpy as np
 
@@ -139,6 +143,19 @@ class ModalSplit:
         _lib.check(_lib.lib().ivk_patch_gather_blocks(patches.system.desc, dev["desc"], kmax,
                                                       ptr(Ms), ptr(Ks), ptr(Cb), stream()),
                    "patch_gather_blocks")
+        if kmax <= 32 and os.environ.get("IVK_MODAL_SETUP", "") != "cusolver":
+            # K7m: Cholesky + Jacobi eigensolver + record assembly in one kernel,
+            # a warp per patch (ivk_modal_factor); larger patches (3-D, k = 65)
+            # and IVK_MODAL_SETUP=cusolver (the A/B) take the batched
+            # torch.linalg route below
+            flag = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=tdev)
+            _lib.check(_lib.lib().ivk_modal_factor(dev["desc"], kmax, ptr(Ms), ptr(Ks), ptr(Cb),
+                                                   ptr(flag), stream()), "modal_factor")
+            v = int(flag.item())
+            bad = np.flatnonzero(ks == 0).tolist()
+            if v != 2 ** 31 - 1:
+                bad.extend(np.flatnonzero(np.asarray(t.order) == v).tolist())
+            return bad
         A = torch.from_numpy(self.A).to(tdev)
         s, nc, dt = self.s, self.nc, self.dt
         eye = torch.eye(s, dtype=torch.float64, device=tdev)

@@ -341,6 +341,25 @@ class StageSystem:
         desc.conv_s = t["conv_s"].data_ptr() if "conv_s" in t else None
         desc.nnz_s = nnz_s
         desc.ncomp = self.nc
+        # locality order of the SELL slices (2-D, coordinates known): pressure
+        # slices first (long rows), both kinds along a Hilbert curve through
+        # the slice centroids, so a CTA's eight slices gather overlapping x
+        xy = getattr(b, "node_xy", None)
+        if self.nc == 2 and xy is not None and os.environ.get("IVK_K1_ORDER", "0") != "0":
+            from .k1tiles import hilbert_key
+
+            def centroid_order(pts, width):
+                n = len(pts)
+                sl = np.arange(n) // width
+                cnt = np.bincount(sl)
+                c = np.column_stack([np.bincount(sl, weights=pts[:, d]) / cnt for d in range(2)])
+                return np.argsort(hilbert_key(c), kind="stable")
+            nsv = (self.n_nodes + 15) // 16
+            ordv = centroid_order(xy[:self.n_nodes], 16)
+            ordp = centroid_order(xy[:self.n_p], 32) + nsv
+            t["k1_order"] = upload(np.concatenate([ordp, ordv]), np.int32)
+            desc.k1_order = t["k1_order"].data_ptr()
+            desc.k1_order_n = len(ordp) + len(ordv)
         tiles = None
         tile_rows = int(os.environ.get("IVK_K1_TILES", "0"))
         if tile_rows > 0 and self.nc == 2 and n_conv == 0:
