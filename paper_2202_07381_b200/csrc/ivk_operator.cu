@@ -65,6 +65,21 @@ struct OpParams {
 // per SM): its software-pipelined gathers need 78 otherwise, and the lost
 // occupancy costs more than the pipelining gains (57 -> 60 us uncapped, 51.6
 // capped, cfg2 fine level).
+// Loads of the operator's own streams (SELL columns and values: read once per
+// apply).  IVK_K1_STREAM=1 marks them evict-first (ld.global.cs) so the L1
+// lines they would take stay with the gathered x.
+#ifndef IVK_K1_STREAM
+#define IVK_K1_STREAM 0
+#endif
+template <class T>
+__device__ __forceinline__ T k1_ld(const T* p) {
+#if IVK_K1_STREAM
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
+
 template <int S, int NC, bool LIST>
 __global__ void __launch_bounds__(256, (NC == 0 && S >= 2) ? 4 : 0) stage_apply_kernel(OpParams op, const double* __restrict__ x,
                                                           const double* b,
@@ -116,8 +131,8 @@ __global__ void __launch_bounds__(256, (NC == 0 && S >= 2) ? 4 : 0) stage_apply_
         for (int u = 0; u < U; ++u) {
           const int ee = e0 + j + 16 * u;
           const bool ok = ee < e1;
-          cl[u] = ok ? op.p2_scol[ee] : -1;
-          mk[u] = ok ? op.p2_smk[ee] : make_double2(0.0, 0.0);
+          cl[u] = ok ? k1_ld(op.p2_scol + ee) : -1;
+          mk[u] = ok ? k1_ld(op.p2_smk + ee) : make_double2(0.0, 0.0);
         }
         for (int e = e0 + j; e < e1; e += 16 * U) {
           double uu[U][S];
@@ -131,8 +146,8 @@ __global__ void __launch_bounds__(256, (NC == 0 && S >= 2) ? 4 : 0) stage_apply_
           for (int u = 0; u < U; ++u) {
             const int ee = e + 16 * (U + u);
             const bool ok = ee < e1;
-            cn[u] = ok ? op.p2_scol[ee] : -1;
-            mn[u] = ok ? op.p2_smk[ee] : make_double2(0.0, 0.0);
+            cn[u] = ok ? k1_ld(op.p2_scol + ee) : -1;
+            mn[u] = ok ? k1_ld(op.p2_smk + ee) : make_double2(0.0, 0.0);
           }
 #pragma unroll
           for (int u = 0; u < U; ++u)
@@ -155,8 +170,8 @@ __global__ void __launch_bounds__(256, (NC == 0 && S >= 2) ? 4 : 0) stage_apply_
           for (int u = 0; u < U; ++u) {
             const int ee = e + 16 * u;
             const bool ok = ee < e1;
-            cl[u] = ok ? op.p2_scol[ee] : -1;
-            mk[u] = ok ? op.p2_smk[ee] : make_double2(0.0, 0.0);
+            cl[u] = ok ? k1_ld(op.p2_scol + ee) : -1;
+            mk[u] = ok ? k1_ld(op.p2_smk + ee) : make_double2(0.0, 0.0);
           }
           double uu[U][S];
 #pragma unroll
@@ -221,8 +236,8 @@ __global__ void __launch_bounds__(256, (NC == 0 && S >= 2) ? 4 : 0) stage_apply_
           for (int u = 0; u < U; ++u) {
             const int ee = e + 16 * u;
             const bool ok = ee < f1;
-            q[u] = ok ? op.b_scol[ee] : -1;
-            const double2 bv = ok ? op.b_sval[ee] : make_double2(0.0, 0.0);
+            q[u] = ok ? k1_ld(op.b_scol + ee) : -1;
+            const double2 bv = ok ? k1_ld(op.b_sval + ee) : make_double2(0.0, 0.0);
             bc[u] = c ? bv.y : bv.x;
           }
           double pp[U][S];
@@ -273,8 +288,8 @@ __global__ void __launch_bounds__(256, (NC == 0 && S >= 2) ? 4 : 0) stage_apply_
       for (int u = 0; u < U; ++u) {
         const int ee = e + 32 * u;
         const bool ok = ee < e1;
-        nn[u] = ok ? op.bt_scol[ee] : -1;
-        bv[u] = ok ? op.bt_sval[ee] : make_double2(0.0, 0.0);
+        nn[u] = ok ? k1_ld(op.bt_scol + ee) : -1;
+        bv[u] = ok ? k1_ld(op.bt_sval + ee) : make_double2(0.0, 0.0);
       }
       double2 xv[U][S];
 #pragma unroll

@@ -1452,8 +1452,12 @@ __device__ __forceinline__ uint32_t modal_slot(uint32_t R, uint32_t Rp, int j, i
 // KTX = ceil(kmax / 4) K-steps of 4 nodes run for every patch, branch-free:
 // rows of R / T past a patch's k are exact zeros, so smaller patches simply
 // multiply zeros (no divergent DMMA regions, loads pipelined across steps).
+#ifndef IVK_K3M_MAXT
+#define IVK_K3M_MAXT (kApplyWarps * 32)
+#define IVK_K3M_MINB 1
+#endif
 template <int S, int NC, int KP, int KTX>
-__global__ void __launch_bounds__(kApplyWarps * 32) patch_apply_modal_tc_kernel(
+__global__ void __launch_bounds__(IVK_K3M_MAXT, IVK_K3M_MINB) patch_apply_modal_tc_kernel(
     PatchParams pd, ModalParams mp, const double* __restrict__ r, double* __restrict__ local,
     int kmax) {
   extern __shared__ __align__(16) double modal_sm[];
@@ -2919,6 +2923,7 @@ int ivk_patch_apply(const ivk_patch_desc* pd, const double* r, double* local, vo
       }
     }
     if (nw > kApplyWarps) nw = kApplyWarps;
+    if (nw > IVK_K3M_MAXT / 32) nw = IVK_K3M_MAXT / 32;
     if (nw < 1) nw = 1;
     IVK_REQUIRE(seg <= 200 * 1024, "modal patch (k = %d) exceeds shared memory", kmax);
     const size_t smem = seg * nw;
