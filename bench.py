@@ -528,6 +528,29 @@ def run_ours(args, rank, world, local):
         return t_step, t_k3, launches, (clk.summary() if clk else None), \
             bool(torch.isfinite(x).all())
 
+    def time_kernels(pat, steps=200):
+        """Average launch time of each sweep kernel (K1, K3, K4) from CUDA
+        events around every launch, outside the headline loop."""
+        dev = pat.device_data()
+        x = torch.zeros_like(b)
+        r = torch.zeros_like(b)
+        w = pat.weights("pou")
+        k1 = L.ivk_general_apply if is_mhd else L.ivk_stage_apply
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+        for k in range(-3, steps):
+            ev = evs[max(k, 0)]
+            st = stream()
+            ev[0].record()
+            _lib.check(k1(S.desc, ptr(x), ptr(b), ptr(r), st), "K1")
+            ev[1].record()
+            _lib.check(L.ivk_patch_apply(dev["desc"], ptr(r), ptr(dev["local"]), st), "K3")
+            ev[2].record()
+            _lib.check(L.ivk_patch_combine(dev["desc"], ptr(dev["local"]), ptr(x), 1.0, om,
+                                           ptr(w), ptr(x), None, st), "K4")
+            ev[3].record()
+        torch.cuda.synchronize()
+        return [float(np.mean([e[i].elapsed_time(e[i + 1]) for e in evs])) / 1e3 for i in range(3)]
+
     # V-cycles (graph-captured) in both smoother modes
     def time_vcycles(h):
         h.use_graph = True
@@ -664,6 +687,16 @@ def run_ours(args, rank, world, local):
     sweep_bytes, k3_canon, sm, sm2 = algorithmic_bytes(S, fine.tables)
     k3_bytes = k3_canon - 8 * sm2 + 8 * fine.inv_size   # executed formulation
     sweep_exec = sweep_bytes - 8 * sm2 + 8 * fine.inv_size
+    # every sweep kernel against the HBM roofline (north_star: SpMV, gather and
+    # patch apply): algorithmic bytes per launch / event time
+    tk1, tk3, tk4 = time_kernels(fine)
+    k1_bytes = sweep_bytes - 8 * sm2 - 4 * sm                      # operator + x, b, r
+    k4_bytes = 12 * int(fine.device_data()["local"].numel()) + 4 * S.dim + 24 * S.dim
+    kernels = {name: {"ms": 1e3 * t, "bytes_per_launch": int(nb),
+                      "achieved_gbs": nb / t / 1e9, "frac": nb / t / 1e9 / hbm}
+               for name, t, nb in (("k1_stage_apply", tk1, k1_bytes),
+                                   ("k3_patch_apply", tk3, k3_bytes),
+                                   ("k4_combine", tk4, k4_bytes))}
 
     # The reference's own formulation (one (s b)^2 inverse per patch) for comparison.
     formulations = {fine.mode: {"ms_per_sweep": 1e3 * t_step, "k3_ms": 1e3 * t_k3,
@@ -824,6 +857,7 @@ def run_ours(args, rank, world, local):
                          "sweep_achieved_gbs": sweep_exec / t_step / 1e9,
                          "sweep_frac": sweep_exec / t_step / 1e9 / hbm,
                          "canonical_equiv_gbs": sweep_bytes / t_step / 1e9},
+            "kernels": kernels,
             "formulations": formulations,
             "cpu_baseline": cpu,
             "e2e": {"value": world / t_e2e, "unit": "sweeps/s",

@@ -1452,12 +1452,17 @@ __device__ __forceinline__ uint32_t modal_slot(uint32_t R, uint32_t Rp, int j, i
 // KTX = ceil(kmax / 4) K-steps of 4 nodes run for every patch, branch-free:
 // rows of R / T past a patch's k are exact zeros, so smaller patches simply
 // multiply zeros (no divergent DMMA regions, loads pipelined across steps).
-#ifndef IVK_K3M_MAXT
+// A/B knob: -DIVK_K3M_MAXT=160 -DIVK_K3M_MINB=4 caps the kernel at 96 registers
+// (20 warps/SM): measured slower than the uncapped 98 (16 warps/SM), DESIGN §9.
+// (An explicit minBlocks of 1 is NOT neutral: ptxas then spends 138 registers.)
+#ifdef IVK_K3M_MAXT
+#define IVK_K3M_BOUNDS __launch_bounds__(IVK_K3M_MAXT, IVK_K3M_MINB)
+#else
 #define IVK_K3M_MAXT (kApplyWarps * 32)
-#define IVK_K3M_MINB 1
+#define IVK_K3M_BOUNDS __launch_bounds__(kApplyWarps * 32)
 #endif
 template <int S, int NC, int KP, int KTX>
-__global__ void __launch_bounds__(IVK_K3M_MAXT, IVK_K3M_MINB) patch_apply_modal_tc_kernel(
+__global__ void IVK_K3M_BOUNDS patch_apply_modal_tc_kernel(
     PatchParams pd, ModalParams mp, const double* __restrict__ r, double* __restrict__ local,
     int kmax) {
   extern __shared__ __align__(16) double modal_sm[];
