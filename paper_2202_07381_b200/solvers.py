@@ -1207,6 +1207,7 @@ class _KrylovWorkspace:
         self.scal = torch.zeros(4, **f64)              # norm / est scratch
         self.red = _lib.reduction_scratch()
         self.host = torch.zeros(4, dtype=torch.float64).pin_memory()
+        self.events = [torch.cuda.Event(), torch.cuda.Event()]
 
 
 def _fgmres_device(op_apply, b, precond, x0, rtol, atol, maxiter, restart):
@@ -1279,7 +1280,20 @@ def _fgmres_device(op_apply, b, precond, x0, rtol, atol, maxiter, restart):
         _lib.check(L.ivk_axpby(n, 1.0 / beta, ptr(ws.r), 0.0, None, ptr(ws.V[0]), st), "scale")
         g.zero_()
         g[0:1].fill_(beta)
+        # Arnoldi steps are enqueued one ahead of the convergence test: step
+        # j's residual estimate is copied to a pinned slot behind it in stream
+        # order and read while step j + 1 already runs, so the device never
+        # idles on the host's read-back.  Close to the tolerance (last known
+        # estimate within 100x) the test turns synchronous again, so a step is
+        # only ever enqueued in vain if the estimate drops by more than 100x
+        # in one step -- and then it is simply not counted: it writes Z[j],
+        # V[j+1], column j of H and g[j..j+1], none of which the solution over
+        # the first j columns reads.  Same decisions, same counts, same
+        # history as the step-by-step loop.
         k = 0
+        done = False
+        last_est = beta
+        pending = None          # (step index, event) whose estimate is in flight
         for j in range(m):
             if pre_to is not None:
                 pre_to(ws.V[j], ws.Z[j])
@@ -1294,12 +1308,42 @@ def _fgmres_device(op_apply, b, precond, x0, rtol, atol, maxiter, restart):
                                  ptr(ws.red), st), "mgs")
             _lib.check(L.ivk_givens(j, ld, ptr(ws.H), ptr(cs), ptr(sn), ptr(g), ptr(ws.scal[1:]),
                                     st), "givens")
-            k = j + 1
+            slot = 2 + (j & 1)
+            ws.host[slot:slot + 1].copy_(ws.scal[1:2], non_blocking=True)
+            ev = ws.events[j & 1]
+            ev.record()
+            if pending is not None:
+                # the previous step's estimate (complete by now or soon: this
+                # step's work is already queued behind it)
+                pj, pev = pending
+                pev.synchronize()
+                est = float(ws.host[2 + (pj & 1)])
+                k = pj + 1
+                stats.iterations += 1
+                stats.residual_norms.append(est)
+                last_est = est
+                if est <= tol or stats.iterations >= maxiter:
+                    done = True       # step j was enqueued in vain
+                    break
+            pending = (j, ev)
+            last = j == m - 1 or stats.iterations + 1 >= maxiter
+            if last or last_est <= 100.0 * tol:
+                ev.synchronize()
+                est = float(ws.host[slot])
+                pending = None
+                k = j + 1
+                stats.iterations += 1
+                stats.residual_norms.append(est)
+                last_est = est
+                if est <= tol or stats.iterations >= maxiter:
+                    done = True
+                    break
+        if pending is not None and not done:   # (m steps enqueued, last one unread)
+            pj, pev = pending
+            pev.synchronize()
+            k = pj + 1
             stats.iterations += 1
-            est = read(1)
-            stats.residual_norms.append(est)
-            if est <= tol or stats.iterations >= maxiter:
-                break
+            stats.residual_norms.append(float(ws.host[2 + (pj & 1)]))
         _lib.check(L.ivk_hessenberg_solve(k, ld, ptr(ws.H), ptr(g), ptr(ws.y), st), "triu solve")
         _lib.check(L.ivk_lincomb(n, ptr(ws.Z), n, k, ptr(ws.y), ptr(x), st), "lincomb")
         true_norm = residual_norm(x)

@@ -23,6 +23,23 @@ def main(name, n, mode="kron"):
     mg, S = disc.build_mg(tab, cfg["dt"], SmootherSpec(), convection=conv, patch_mode=mode)
     pat = mg.levels[-1].patches
     dev = pat.device_data()
+    if os.environ.get("IVK_EXP_SHARE_RECORDS") and pat.mode == "modal":
+        # experiment: patches with bitwise identical records read one copy
+        from paper_2202_07381_b200.modal import _bitwise_classes
+        ks = np.diff(pat.tables.node_off)
+        off = np.asarray(pat.inv_off, dtype=np.int64).copy()
+        ncls = 0
+        for k in np.unique(ks):
+            sel = np.flatnonzero(ks == k)
+            rec = pat.modal.record_doubles(int(k))
+            first, count = int(sel[0]), len(sel)
+            o0 = int(off[first])
+            recs = dev["inv"][o0:o0 + count * rec].view(count, rec)
+            rep, inv = _bitwise_classes(recs)
+            ncls += len(rep)
+            off[first:first + count] = o0 + rep.cpu().numpy()[inv.cpu().numpy()] * rec
+        dev["inv_off"].copy_(torch.from_numpy(off).to(dev["inv_off"].device))
+        print(f"shared records: {ncls} classes for {pat.num_patches} patches")
     b_h = np.random.default_rng(cfg["seed"]).uniform(-1, 1, S.dim)
     b_h[S.constrained_stage_dofs()] = 0.0
     S.project_pressure_means(b_h)
