@@ -3139,7 +3139,10 @@ int ivk_patch_factor(const ivk_operator_desc* op, const ivk_patch_desc* pd, int3
     set_error("ivk_patch_factor: patch size %d > 512 unsupported", dmax);
     return IVK_EUNSUPPORTED;
   }
-  const size_t smem = (size_t)dmax * ((dmax + 3) & ~3) * sizeof(double);
+  // d x ld doubles for the register kernel (d <= 128: it leaves Inv^T with the
+  // store's leading dimension in shared memory), d x d for the shared-memory one
+  const size_t smem = dmax <= 128 ? (size_t)dmax * ((dmax + 3) & ~3) * sizeof(double)
+                                  : (size_t)dmax * dmax * sizeof(double);
   if (op->ncomp == 3 || smem > 220 * 1024) {
     IVK_REQUIRE(op->n_conv == 0, "large-patch factorisation supports no convection");
     FactorParams f = make_factor_params(op);

@@ -97,9 +97,7 @@ def _coo_to_csr(rows, cols, vals, n_rows, n_cols, canonical=False):
     ukey = key[first]
     urow = ukey // n_cols
     col = (ukey % n_cols).astype(np.int32)
-    rowptr = np.zeros(n_rows + 1, dtype=np.int64)
-    np.add.at(rowptr, urow + 1, 1)
-    rowptr = np.cumsum(rowptr)
+    rowptr = np.concatenate(([0], np.cumsum(np.bincount(urow, minlength=n_rows)))).astype(np.int64)
     return rowptr, col, summed
 
 
