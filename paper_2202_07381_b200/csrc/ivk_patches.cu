@@ -1506,6 +1506,14 @@ __global__ void IVK_K3M_BOUNDS patch_apply_modal_tc_kernel(
   const int pbeg = blockIdx.x * chunk;
   const int pend = min(pd.num_patches, pbeg + chunk);
   int p = pbeg + warp;
+  // byte offset, inside an R buffer, of fragment-layout entry lane + 32 u (a
+  // velocity entry: node*NA + q); the same for every patch
+  uint32_t lslot[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = lane + 32 * u, al = j / NA;
+    lslot[u] = 8u * modal_tpos<NA>(al, j - al * NA);
+  }
   int rz0 = 0, rz1 = 0;   // leading rows of R[0] / R[1] a gather may have left non-zero
   if (lane == 0 && p < pend) {
     const int k0 = pd.node_off[p + 1] - pd.node_off[p];
@@ -1556,8 +1564,10 @@ __global__ void IVK_K3M_BOUNDS patch_apply_modal_tc_kernel(
       const int nak = NA * pn_k;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (pf_idx[u] >= 0)
-          cp_async8(modal_slot<NA>(RN_u, RPN_u, lane + 32 * u, nak), r + pf_idx[u]);
+        if (pf_idx[u] >= 0) {
+          const int j = lane + 32 * u;
+          cp_async8(j < nak ? RN_u + lslot[u] : RPN_u + 8u * (j - nak), r + pf_idx[u]);
+        }
       for (int j = 128 + lane; j < pn_m; j += 32)
         cp_async8(modal_slot<NA>(RN_u, RPN_u, j, nak), r + __ldg(pd.idx + pn_off + j));
       cp_async_commit();
@@ -1618,17 +1628,21 @@ __global__ void IVK_K3M_BOUNDS patch_apply_modal_tc_kernel(
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           const int q0 = 8 * n + 2 * gk;
+          // rows past k (their A columns were record tails: finite garbage)
+          // are stored as the exact zeros the U GEMM's unpredicated A
+          // columns must meet
+          const bool live = 8 * m + gq < k;
+          const double t0 = live ? d[m][n][0] : 0.0, t1 = live ? d[m][n][1] : 0.0;
           if constexpr (SWZ && NA % 2 == 0) {
             // the pair (q0, q0 + 1) stays one aligned 16-byte slot, swapped
             // where sw(row) is odd
             const int row = 8 * m + gq, sw = modal_sw(row);
             if (q0 < NA)
               *reinterpret_cast<double2*>(t + row * 8 + ((q0 ^ sw) & ~1)) =
-                  (sw & 1) ? make_double2(d[m][n][1], d[m][n][0])
-                           : make_double2(d[m][n][0], d[m][n][1]);
+                  (sw & 1) ? make_double2(t1, t0) : make_double2(t0, t1);
           } else {
-            if (q0 < NA) t[modal_tpos<NA>(8 * m + gq, q0)] = d[m][n][0];
-            if (q0 + 1 < NA) t[modal_tpos<NA>(8 * m + gq, q0 + 1)] = d[m][n][1];
+            if (q0 < NA) t[modal_tpos<NA>(8 * m + gq, q0)] = t0;
+            if (q0 + 1 < NA) t[modal_tpos<NA>(8 * m + gq, q0 + 1)] = t1;
           }
         }
     }
@@ -1700,11 +1714,7 @@ __global__ void IVK_K3M_BOUNDS patch_apply_modal_tc_kernel(
 #pragma unroll
         for (int a = 0; a < S; ++a)
           t[modal_tpos<NA>(im, dd * S + a)] = fma(-dt * cc[dd], e[a], wv[dd * S + a]);
-    } else if (im < KP) {
-      // rows past k: exact zeros for the U GEMM's unpredicated A columns
-#pragma unroll
-      for (int q = 0; q < NA; ++q) t[modal_tpos<NA>(im, q)] = 0.0;
-    }
+    }   // (rows past k already hold the zeros the T store wrote)
     __syncwarp();
     // U = W V; each lane stores its D fragment entries (node 8m+gq, columns
     // 8n+2gk, +1) straight to their fragment-layout slots
