@@ -842,10 +842,11 @@ def run_ours(args, rank, world, local):
             "stage_dof_updates_per_s": world * S.dim / t_step,
             "roofline": {"bound": "hbm", "kernel": f"ivk patch_apply (K2+K3, {fine.mode})",
                          "limiter": ("modal: 0.23 GB of records per sweep -- bound by the "
-                                     "SM's shared-memory/LSU pipe (ncu: ~65% of peak LSU "
+                                     "SM's shared-memory/LSU pipe (ncu: 68% of peak LSU "
                                      "wavefronts, tensor-core fragment traffic) and per-patch "
-                                     "dependent phases, not HBM; kron's HBM-bound K3 is in "
-                                     "formulations.kron")
+                                     "dependent phases, not HBM (with the records served "
+                                     "from L2 it runs 93.0 vs 94.4 us, DESIGN.md 9.0); "
+                                     "kron's HBM-bound K3 is in formulations.kron")
                          if fine.mode == "modal" else "hbm stream of the inverse store",
                          "achieved": k3_bytes / t_k3 / 1e9, "peak": hbm, "unit": "GB/s",
                          "frac": k3_bytes / t_k3 / 1e9 / hbm,
