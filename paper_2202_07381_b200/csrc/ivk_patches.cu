@@ -1452,6 +1452,11 @@ __device__ __forceinline__ uint32_t modal_slot(uint32_t R, uint32_t Rp, int j, i
 // KTX = ceil(kmax / 4) K-steps of 4 nodes run for every patch, branch-free:
 // rows of R / T past a patch's k are exact zeros, so smaller patches simply
 // multiply zeros (no divergent DMMA regions, loads pipelined across steps).
+// A/B knob: -DIVK_K3M_CH=2 splits each GEMM row tile's K steps into two
+// independent accumulator chains (measured below).
+#ifndef IVK_K3M_CH
+#define IVK_K3M_CH 1
+#endif
 // A/B knob: -DIVK_K3M_MAXT=160 -DIVK_K3M_MINB=4 caps the kernel at 96 registers
 // (20 warps/SM): measured slower than the uncapped 98 (16 warps/SM), DESIGN §9.
 // (An explicit minBlocks of 1 is NOT neutral: ptxas then spends 138 registers.)
@@ -1609,6 +1614,13 @@ __global__ void IVK_K3M_BOUNDS patch_apply_modal_tc_kernel(
       for (int m = 0; m < MT; ++m)
 #pragma unroll
         for (int n = 0; n < NT; ++n) d[m][n][0] = d[m][n][1] = 0.0;
+#if IVK_K3M_CH > 1
+      double d2[MT][NT][2];   // second accumulator chain (odd K steps)
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) d2[m][n][0] = d2[m][n][1] = 0.0;
+#endif
 #pragma unroll
       for (int kt = 0; kt < KTX; ++kt) {
         const int al = 4 * kt + gk;
@@ -1619,9 +1631,24 @@ __global__ void IVK_K3M_BOUNDS patch_apply_modal_tc_kernel(
         for (int m = 0; m < MT; ++m) {
           const double a = W[al * ld + 8 * m + gq];   // rows al >= k meet R's zero rows
 #pragma unroll
-          for (int n = 0; n < NT; ++n) dmma884(d[m][n][0], d[m][n][1], a, b[n]);
+          for (int n = 0; n < NT; ++n) {
+#if IVK_K3M_CH > 1
+            if (kt & 1) dmma884(d2[m][n][0], d2[m][n][1], a, b[n]);
+            else
+#endif
+            dmma884(d[m][n][0], d[m][n][1], a, b[n]);
+          }
         }
       }
+#if IVK_K3M_CH > 1
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          d[m][n][0] += d2[m][n][0];
+          d[m][n][1] += d2[m][n][1];
+        }
+#endif
       __syncwarp();   // every lane's R reads are done: T overwrites R in place
 #pragma unroll
       for (int m = 0; m < MT; ++m)
@@ -1724,6 +1751,13 @@ __global__ void IVK_K3M_BOUNDS patch_apply_modal_tc_kernel(
       for (int m = 0; m < MT; ++m)
 #pragma unroll
         for (int n = 0; n < NT; ++n) d[m][n][0] = d[m][n][1] = 0.0;
+#if IVK_K3M_CH > 1
+      double d2[MT][NT][2];
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) d2[m][n][0] = d2[m][n][1] = 0.0;
+#endif
 #pragma unroll
       for (int kt = 0; kt < KTX; ++kt) {
         const int i = 4 * kt + gk;
@@ -1734,9 +1768,24 @@ __global__ void IVK_K3M_BOUNDS patch_apply_modal_tc_kernel(
         for (int m = 0; m < MT; ++m) {
           const double a = W[(8 * m + gq) * ld + i];   // columns i >= k meet t's zero rows
 #pragma unroll
-          for (int n = 0; n < NT; ++n) dmma884(d[m][n][0], d[m][n][1], a, b[n]);
+          for (int n = 0; n < NT; ++n) {
+#if IVK_K3M_CH > 1
+            if (kt & 1) dmma884(d2[m][n][0], d2[m][n][1], a, b[n]);
+            else
+#endif
+            dmma884(d[m][n][0], d[m][n][1], a, b[n]);
+          }
         }
       }
+#if IVK_K3M_CH > 1
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          d[m][n][0] += d2[m][n][0];
+          d[m][n][1] += d2[m][n][1];
+        }
+#endif
       double* lp = local + off;
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
@@ -1795,6 +1844,11 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
   constexpr int MT = KP / 8, KT = KP / 4;
   constexpr int NTH = kModalCtaWarps * 32;
   constexpr int PF = 4;             // prefetched r values per thread (m <= 512)
+#ifndef IVK_MODAL_CTA_CH
+#define IVK_MODAL_CTA_CH 3
+#endif
+  constexpr int CH = IVK_MODAL_CTA_CH;   // accumulator chains per GEMM row tile
+  static_assert(KT % CH == 0, "the K steps must split evenly into the chains");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, gk = lane & 3;
   const int recmax = modal_rec(S, NC, kmax);
@@ -1873,17 +1927,35 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
     // T = W^T R: warp w takes mode tiles w, w + 4, ...
     for (int m = warp; m < MT; m += kModalCtaWarps) {
       if (8 * m >= k) break;
+      // CH independent accumulator chains over the K steps (one chain of
+      // KT = 18 dependent DMMAs is latency-bound: 584 -> 513 us at cfg4),
+      // summed in a fixed order
+      double dc[CH][NT][2];
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) dc[c][n][0] = dc[c][n][1] = 0.0;
+      const int i = 8 * m + gq;
+      for (int kt0 = 0; kt0 < KT && 4 * kt0 < k; kt0 += CH) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const int al = 4 * (kt0 + c) + gk;      // < KP: KT is a multiple of CH
+          const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+#pragma unroll
+          for (int n = 0; n < NT; ++n)
+            dmma884(dc[c][n][0], dc[c][n][1], a, R[al * NW + 8 * n + gq]);
+        }
+      }
       double d[NT][2];
 #pragma unroll
-      for (int n = 0; n < NT; ++n) d[n][0] = d[n][1] = 0.0;
-      const int i = 8 * m + gq;
-#pragma unroll 4
-      for (int kt = 0; kt < KT; ++kt) {
-        if (4 * kt >= k) break;
-        const int al = 4 * kt + gk;
-        const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+      for (int n = 0; n < NT; ++n) {
+        d[n][0] = dc[0][n][0];
+        d[n][1] = dc[0][n][1];
 #pragma unroll
-        for (int n = 0; n < NT; ++n) dmma884(d[n][0], d[n][1], a, R[al * NW + 8 * n + gq]);
+        for (int c = 1; c < CH; ++c) {
+          d[n][0] += dc[c][n][0];
+          d[n][1] += dc[c][n][1];
+        }
       }
 #pragma unroll
       for (int n = 0; n < NT; ++n)
@@ -1978,17 +2050,32 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
     // U = W V: warp w takes node tiles w, w + 4, ...
     for (int m = warp; m < MT; m += kModalCtaWarps) {
       if (8 * m >= k) break;
+      double dc[CH][NT][2];
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) dc[c][n][0] = dc[c][n][1] = 0.0;
+      const int al = 8 * m + gq;
+      for (int kt0 = 0; kt0 < KT && 4 * kt0 < k; kt0 += CH) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const int i = 4 * (kt0 + c) + gk;
+          const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+#pragma unroll
+          for (int n = 0; n < NT; ++n)
+            dmma884(dc[c][n][0], dc[c][n][1], a, t[i * NW + 8 * n + gq]);
+        }
+      }
       double d[NT][2];
 #pragma unroll
-      for (int n = 0; n < NT; ++n) d[n][0] = d[n][1] = 0.0;
-      const int al = 8 * m + gq;
-#pragma unroll 4
-      for (int kt = 0; kt < KT; ++kt) {
-        if (4 * kt >= k) break;
-        const int i = 4 * kt + gk;
-        const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+      for (int n = 0; n < NT; ++n) {
+        d[n][0] = dc[0][n][0];
+        d[n][1] = dc[0][n][1];
 #pragma unroll
-        for (int n = 0; n < NT; ++n) dmma884(d[n][0], d[n][1], a, t[i * NW + 8 * n + gq]);
+        for (int c = 1; c < CH; ++c) {
+          d[n][0] += dc[c][n][0];
+          d[n][1] += dc[c][n][1];
+        }
       }
       if (al < k) {
 #pragma unroll
