@@ -1861,7 +1861,11 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
   double* Es = t + KP * NW;
   double* gred = Es + KP * S * S;   // kModalCtaWarps x 4 partial sums
   double* pAp = gred + kModalCtaWarps * 4;  // p (4) and A p (4)
-  for (int e = tid; e < 2 * KP * NW + 8 + KP * NW; e += NTH) R0[e] = 0.0;
+  // zero the whole segment once: the tensor-core A loads below are not
+  // predicated, so they read (finite) record tails and the buffers behind
+  // them -- every such value meets an exact zero row of R / t
+  for (int e = tid; e < modal_cta_smem(S, NC, kmax, KP); e += NTH) modal_sm[e] = 0.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // before TMA overwrites
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -1918,6 +1922,11 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
       const int j = tid + NTH * u;
       pf_idx[u] = (pn < pd.num_patches && j < S * pn_blk) ? __ldg(pd.idx + pn_off + j) : -1;
     }
+    // t rows this patch's T store will not reach (a larger patch may have left
+    // values there) must be the zeros the U GEMM's unpredicated A columns meet;
+    // every thread is past the previous patch's reads of t (barrier at the
+    // loop end), and two barriers separate this from the U GEMM
+    for (int e = ((k + 7) & ~7) * NW + tid; e < KP * NW; e += NTH) t[e] = 0.0;
     mbar_wait(&bars[slot], (phase >> slot) & 1u);
     phase ^= 1u << slot;
     const double* W = slot ? buf1 : buf0;
@@ -1940,7 +1949,7 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
           const int al = 4 * (kt0 + c) + gk;      // < KP: KT is a multiple of CH
-          const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+          const double a = W[al * ld + i];        // rows al >= k meet R's zero rows
 #pragma unroll
           for (int n = 0; n < NT; ++n)
             dmma884(dc[c][n][0], dc[c][n][1], a, R[al * NW + 8 * n + gq]);
@@ -1957,9 +1966,13 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
           d[n][1] += dc[c][n][1];
         }
       }
+      // mode rows past k (their A columns were record tails) are stored as the
+      // exact zeros the U GEMM's unpredicated A columns must meet
+      const bool live = i < k;
 #pragma unroll
       for (int n = 0; n < NT; ++n)
-        *reinterpret_cast<double2*>(t + i * NW + 8 * n + 2 * gk) = make_double2(d[n][0], d[n][1]);
+        *reinterpret_cast<double2*>(t + i * NW + 8 * n + 2 * gk) =
+            live ? make_double2(d[n][0], d[n][1]) : make_double2(0.0, 0.0);
     }
     double pf_val[PF];
 #pragma unroll
@@ -2060,7 +2073,7 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
           const int i = 4 * (kt0 + c) + gk;
-          const double a = (al < k && i < k) ? W[al * ld + i] : 0.0;
+          const double a = W[al * ld + i];        // columns i >= k meet t's zero rows
 #pragma unroll
           for (int n = 0; n < NT; ++n)
             dmma884(dc[c][n][0], dc[c][n][1], a, t[i * NW + 8 * n + gq]);
@@ -2101,6 +2114,7 @@ __global__ void __launch_bounds__(kModalCtaWarps * 32) patch_apply_modal_cta_ker
       double* RN = slot ? R0 : R1;
       double* RPN = Rp + 4 * (slot ^ 1);
       for (int e = pn_k * NW + tid; e < KP * NW; e += NTH) RN[e] = 0.0;
+
 #pragma unroll
       for (int u = 0; u < PF; ++u) {
         const int j = tid + NTH * u;
