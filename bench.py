@@ -691,6 +691,10 @@ def run_ours(args, rank, world, local):
     # patch apply): algorithmic bytes per launch / event time
     tk1, tk3, tk4 = time_kernels(fine)
     k1_bytes = sweep_bytes - 8 * sm2 - 4 * sm                      # operator + x, b, r
+    if conv is not None and not is_mhd:
+        # the convection Jacobian's 2x2 block per pattern entry (SURVEY's
+        # canonical count is the Stokes operator's)
+        k1_bytes += 32 * len(S.blocks.col) * len(S._conv_vals)
     k4_bytes = 12 * int(fine.device_data()["local"].numel()) + 4 * S.dim + 24 * S.dim
     kernels = {name: {"ms": 1e3 * t, "bytes_per_launch": int(nb),
                       "achieved_gbs": nb / t / 1e9, "frac": nb / t / 1e9 / hbm}

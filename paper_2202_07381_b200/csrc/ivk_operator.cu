@@ -187,6 +187,47 @@ __global__ void __launch_bounds__(256, (NC == 0 && S >= 2) ? 4 : 0) stage_apply_
             }
         }
         }
+      } else if constexpr (NC == 1) {
+        // one shared Jacobian (Oseen): batches of UJ entries -- their (col,
+        // m/k, J row) loads, then their 2 S gathers of x, in flight together;
+        // each lane reads only its own row (own, other) of the 2x2 block
+#ifndef IVK_K1_UJ
+#define IVK_K1_UJ 4
+#endif
+        constexpr int UJ = IVK_K1_UJ;
+        for (int e = e0 + j; e < e1; e += 16 * UJ) {
+          int cl[UJ];
+          double2 mk[UJ], jr[UJ];
+#pragma unroll
+          for (int u = 0; u < UJ; ++u) {
+            const int ee = e + 16 * u;
+            const bool ok = ee < e1;
+            cl[u] = ok ? op.p2_scol[ee] : -1;
+            mk[u] = ok ? op.p2_smk[ee] : make_double2(0.0, 0.0);
+            // row c of J: (J.x, J.y) or (J.z, J.w)
+            jr[u] = ok ? reinterpret_cast<const double2*>(op.conv_s + ee)[c]
+                       : make_double2(0.0, 0.0);
+          }
+          double uu[UJ][S], vv[UJ][S];
+#pragma unroll
+          for (int u = 0; u < UJ; ++u)
+#pragma unroll
+            for (int t = 0; t < S; ++t) {
+              const long o = t * sd + 2 * (cl[u] >= 0 ? cl[u] : 0);
+              uu[u][t] = cl[u] >= 0 ? x[o + c] : 0.0;
+              vv[u][t] = cl[u] >= 0 ? x[o + (c ^ 1)] : 0.0;
+            }
+#pragma unroll
+          for (int u = 0; u < UJ; ++u) {
+            const double jd = c ? jr[u].y : jr[u].x, jo = c ? jr[u].x : jr[u].y;
+#pragma unroll
+            for (int t = 0; t < S; ++t) {
+              mu[t] = fma(mk[u].x, uu[u][t], mu[t]);
+              ku[t] = fma(mk[u].y, uu[u][t], ku[t]);
+              ku[t] += jd * uu[u][t] + jo * vv[u][t];
+            }
+          }
+        }
       } else
 #pragma unroll 2
       for (int e = e0 + j; e < e1; e += 16) {
