@@ -14,8 +14,27 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: full BASELINE-size case")
 
 
+FULL_SIZE_MODULES = ("test_gpu_fullsize", "test_gpu_fullsize_parity")
+
+
+def _group_full_size_by_config(items):
+    """The full-size modules keep ONE BASELINE config's multi-GB oracle and
+    device hierarchies alive at a time; run each module's cfg2 cases before its
+    cfg3 cases (in their slots of the collection order) so each is built once."""
+    for mod in FULL_SIZE_MODULES:
+        slots = [i for i, it in enumerate(items)
+                 if getattr(it.module, "__name__", "").split(".")[-1] == mod]
+        if not slots:
+            continue
+        rank = lambda it: 0 if "cfg2" in it.name else 1 if "cfg3" in it.name else 2
+        ordered = sorted((items[i] for i in slots), key=rank)      # stable
+        for i, it in zip(slots, ordered):
+            items[i] = it
+
+
 def pytest_collection_modifyitems(config, items):
     import torch
+    _group_full_size_by_config(items)
     if torch.cuda.is_available():
         return
     skip = pytest.mark.skip(reason="no CUDA device")
