@@ -105,6 +105,7 @@ class NSStageNewton:
         self.start = disc.num_levels - len(self.mg.levels)
         self._A = torch.from_numpy(np.asarray(tableau.A, dtype=np.float64))
         self._cmask = None
+        self._host_kb = None
 
     # -- pieces ---------------------------------------------------------------
 
@@ -121,9 +122,14 @@ class NSStageNewton:
         S = self.S0
         un = np.asarray(u_n, dtype=np.float64)
         pn = np.asarray(p_n, dtype=np.float64)
-        cu = S.K @ un + S.B @ pn
+        if self._host_kb is None:
+            # the vector-form scipy blocks are rebuilt from the scalar ones on
+            # every property access (a second per step at cfg3): keep them
+            self._host_kb = (S.K, S.B, S.BT)
+        K, B, BT = self._host_kb
+        cu = K @ un + B @ pn
         cu[S.constrained] = 0.0
-        cp = S.BT @ un
+        cp = BT @ un
         c = np.tile(np.concatenate([cu, cp]), self.s)
         return torch.from_numpy(c).cuda()
 
