@@ -164,8 +164,15 @@ class NSStageNewton:
                 lev.patches.factor()
                 lev.system.mark_host_stale()
         s0 = self.mg.levels[0].system
-        s0.download_convection()
-        self.mg.coarse = CoarseSolver(s0, getattr(self.mg.coarse, "method", "dense"))
+        if getattr(self.mg.coarse, "method", "dense") == "dense":
+            # the coarse operator straight from the re-assembled device operator
+            # (the host route -- download, materialize, SuperLU, n solves --
+            # cost 0.3 s per Newton iteration at cfg3, most of the step)
+            s0.mark_host_stale()
+            self.mg.coarse = CoarseSolver.from_device_operator(s0)
+        else:
+            s0.download_convection()
+            self.mg.coarse = CoarseSolver(s0, self.mg.coarse.method)
         self.mg._graph = None
         self.mg._bufs = None
 

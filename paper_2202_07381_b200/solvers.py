@@ -790,6 +790,43 @@ class CoarseSolver:
         out -= Z @ (Z.T @ out)
         return out
 
+    @classmethod
+    def from_device_operator(cls, system):
+        """Dense coarse operator P (A + Z Z^T)^-1 P formed on the device from
+        the system's CURRENT device operator (the Newton-cadence rebuild: the
+        convection was just re-assembled there): A by applying K1 to the unit
+        vectors (n tiny launches), the inverse by a dense LU with partial
+        pivoting (torch.linalg.inv -> cuSOLVER getrf / getri, setup only), the
+        projections as small GEMMs.  Same operator as the SuperLU route up to
+        rounding (both LUs are backward stable); no host factorisation, no
+        download of the convection.  ``method`` is "dense"."""
+        import torch
+        self = cls.__new__(cls)
+        self.system, self.method, self.lu = system, "dense", None
+        self.Z = system.pressure_nullspace()
+        n = system.dim
+        dev = system.device_data()["tensors"]["cmask"].device
+        eye = torch.eye(n, dtype=torch.float64, device=dev)
+        At = torch.empty((n, n), dtype=torch.float64, device=dev)
+        for j in range(n):
+            system.apply_into(eye[j], None, At[j])           # row j of A^T = A e_j
+        Z = torch.from_numpy(np.ascontiguousarray(self.Z)).to(dev)
+        inv = torch.linalg.inv(At.T + Z @ Z.T)
+        out = inv - (inv @ Z) @ Z.T
+        out -= Z @ (Z.T @ out)
+        ld = (n + 3) & ~3
+        D = torch.zeros((n, ld), dtype=torch.float64, device=dev)
+        D[:, :n] = out
+        d = _lib.CoarseDesc()
+        d.n = n
+        d.stages, d.n_u, d.n_p = system.r, system.n_u, system.n_p
+        t = {"dense": D.reshape(-1)}
+        d.dense = t["dense"].data_ptr()
+        d.dense_ld = ld
+        d.nb = (n + 31) // 32
+        self._dev = {"tensors": t, "desc": d}
+        return self
+
     def tiles(self):
         """Tile-sparse (32 x 32, column-major tiles) copies of the factors."""
         return (tile_factor(self.lu.L, lower=True, invert_lower_diag=True),

@@ -50,8 +50,9 @@ def main(name="cfg3", runs=2):
                                    lev.patches.factor)
     for a in nsn.asm:
         a.assemble_stage = timed("K10 assemble_stage", a.assemble_stage)
-    solvers_cs = solvers.CoarseSolver
-    newton.CoarseSolver = timed("coarse SuperLU rebuild", solvers_cs)
+    solvers.CoarseSolver.from_device_operator = staticmethod(
+        timed("coarse operator rebuild (device)",
+              solvers.CoarseSolver.from_device_operator))
     newton.fgmres = timed("fgmres", solvers.fgmres)
     nsn.residual = timed("residual", nsn.residual)
     nsn.relinearize = timed("relinearize (total)", nsn.relinearize)
