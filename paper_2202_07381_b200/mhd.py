@@ -394,8 +394,8 @@ class MHDDiscretization:
         (u0, B0) -- (n_nodes, 2) nodal P2 values, injected to coarser levels as
         the nodal prefix (nested P2 node numbering, as the reference's
         ``inject_velocity``) -- then refactorise the smoothed levels' patches in
-        place (K7g) and rebuild the coarse direct solve: the Newton-cadence
-        update of config 5, all on the device but the coarse factorisation."""
+        place (K7g) and re-form the coarse operator (on the device for the dense
+        coarse method): the Newton-cadence update of config 5."""
         from .solvers import coarse_direct_solve
         start = self.num_levels - len(mg.levels)
         for lv, lev in enumerate(mg.levels):
@@ -404,7 +404,13 @@ class MHDDiscretization:
                 lev.patches.factor()
                 lev.system.mark_host_stale()
         s0 = mg.levels[0].system
-        s0.download_operator()
-        mg.coarse = coarse_direct_solve(s0)
+        if getattr(mg.coarse, "method", "dense") == "dense":
+            # coarse operator straight from the re-assembled device operator
+            from .solvers import CoarseSolver
+            s0.mark_host_stale()
+            mg.coarse = CoarseSolver.from_device_operator(s0)
+        else:
+            s0.download_operator()
+            mg.coarse = coarse_direct_solve(s0, mg.coarse.method)
         mg._graph = None
         mg._bufs = None
