@@ -1119,7 +1119,10 @@ class MGHierarchyOp:
         GPU for every level from the device velocity ``u`` (nodal injection
         u_l = u[:2 n_l], bench.py:178-185), refactorise every level's patches
         in place (K7) and re-factor the coarsest operator (host SuperLU, as the
-        reference's coarse_direct_solve)."""
+        reference's coarse_direct_solve -- its result is pinned against a
+        hierarchy built from scratch at 1e-9 where the coarse operator has
+        cond ~1e8; the Newton drivers, which only need a preconditioner, take
+        the device route ``CoarseSolver.from_device_operator`` instead)."""
         if len(assemblers) != len(self.levels):
             raise ValueError("one ConvectionAssembler per level required")
         for k, (lev, asm) in enumerate(zip(self.levels, assemblers)):
